@@ -1,0 +1,153 @@
+/*
+ * hsrq.h -- C ABI of libhsrq_b200.so, the B200 implementation of the batched
+ * shifted-Hessenberg robust RQ solve (H - lambda_j I) x_j = s_j b_j
+ * (arXiv 2101.05063) behind the reference hessrq package's inverse-iteration
+ * seam.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/hessrq):
+ *
+ *   hsrq_solve_group   _solve_group, inviter.py:91-106 (tiled_reduce,
+ *                      reduce.py:39-171, + robust_tiled_solve(mode="eigvec"),
+ *                      backsolve.py:329-347) and, with mode=0 / robust=0,
+ *                      the dhsrq3/chsrq3 engine backsolve.py:350-388.
+ *                      Returns what SolutionBlock (core.py:251-260) carries:
+ *                      x, per-column alpha, segment scales, represented norms.
+ *   hsrq_protect_update_batch   protect_update, _kernels/numba_backend.py:47-67
+ *   hsrq_hypot_batch            libm hypot as bound by numba (every rotation)
+ *   hsrq_tile_diag              reduce_diag + solve_rsolve (numba_backend.py:
+ *                               75-106, 133-195) and creduce_diag +
+ *                               csolve_crsolve (:420-464, :554-576) on one
+ *                               diagonal tile: the tile-level operator API
+ *                               (_kernels/__init__.py) for parity tests.
+ *
+ * Conventions: every pointer argument is DEVICE memory unless its name ends
+ * in _host.  Plain C types only; `stream` is a cudaStream_t passed as void*.
+ * All calls are stream-ordered and re-entrant per stream; the library keeps
+ * no global state besides cached device attributes.  H is never written.
+ *
+ * Shift / column layout.  A solve group holds m_cplx complex shifts
+ * (Im > 0; the caller conjugates, as chsrq3in does, inviter.py:164-183)
+ * followed by m_real real shifts: shift q < m_cplx is complex and owns the
+ * two real columns 2q (re) and 2q+1 (im); shift q >= m_cplx is real and owns
+ * column 2*m_cplx + (q - m_cplx).  ncol = 2*m_cplx + m_real.  Column-major
+ * n x ncol blocks (X, B) use leading dimension ldx / ldb.
+ *
+ * Scale factors are returned as int32 log2 exponents: the reference's double
+ * is ldexp(1, e).  This is bit-identical to the reference wherever
+ * e >= -1074 and keeps working where the reference underflows to 0
+ * (SURVEY.md §0 finding 6).
+ */
+#ifndef HSRQ_B200_H
+#define HSRQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HSRQ_KIND_DEGENERATE 1 /* numba_backend.py:17 */
+#define HSRQ_KIND_SINGULAR 2   /* numba_backend.py:18 */
+
+/* Error codes (negative returns). */
+#define HSRQ_ERR_CONFIG (-1)   /* b_r outside [1, 128], n < 1, bad sizes */
+#define HSRQ_ERR_WORKSPACE (-2) /* workspace too small */
+#define HSRQ_ERR_CUDA (-3)     /* a CUDA call failed; see hsrq_last_error() */
+
+/* Library version string and the last CUDA error text (thread-local). */
+const char* hsrq_version(void);
+const char* hsrq_last_error(void);
+
+/* Bytes of device workspace hsrq_solve_group needs. */
+size_t hsrq_workspace_bytes(int64_t n, int32_t b_r, int64_t m_cplx, int64_t m_real);
+
+/*
+ * Robust tiled RQ solve for one group of shifts (see header comment).
+ *
+ *  H        n x n column-major, leading dimension ldh (>= n)
+ *  lam_re   m_cplx + m_real shift real parts (complex first, then real)
+ *  lam_im   imaginary parts (entries for real shifts are ignored)
+ *  B        right-hand sides: b_broadcast = 0 -> n x ncol column-major
+ *           (ldb); b_broadcast = 1 -> one real n-vector used for every
+ *           column (imaginary parts 0), the start vector _iterate repeats
+ *           (inviter.py:127-133)
+ *  X        out, n x ncol column-major (ldx); may alias B when ldb == ldx
+ *  c_re, c_im, s   out, recorded rotations, n x (m_cplx + m_real) column-major
+ *           (ldc), row j mixing columns j-1 and j (GivensTable, core.py:168-179);
+ *           c_im is written as 0 for real shifts
+ *  seg_exp  out, N x (m_cplx + m_real) int32, N = ceil(n / b_r): segment
+ *           scale exponents (ScalingMatrix, core.py:234-248), row-major by tile
+ *  alpha_exp out, per-shift column scale exponent (alpha_min, or the solve
+ *           mode's extra guard, numba_backend.py:326-375)
+ *  norms    out, represented 2-norm as the reference's double (may be +inf)
+ *  log2norm out, log2 of the represented norm (finite where norms is inf)
+ *  fail     out, per shift: 0, or (phase << 56) | (tile << 24) | row of the
+ *           first failure (phase 1 = degenerate rotation, 2 = singular factor)
+ *  robust   1 = robust_tiled_solve (Omega = DBL_MAX/2/b_r), 0 = tiled_solve
+ *  mode     1 = eigvec (normalise), 0 = solve
+ *  ws       workspace of >= hsrq_workspace_bytes(...) bytes
+ *
+ * Returns the number of failed shifts (>= 0) after synchronising `stream`,
+ * or a negative HSRQ_ERR_*.
+ */
+int64_t hsrq_solve_group(const double* H, int64_t ldh, int64_t n, int32_t b_r,
+                         const double* lam_re, const double* lam_im, int64_t m_cplx,
+                         int64_t m_real, const double* B, int64_t ldb, int32_t b_broadcast,
+                         double* X, int64_t ldx, double* c_re, double* c_im, double* s,
+                         int64_t ldc, int32_t* seg_exp, int32_t* alpha_exp, double* norms,
+                         double* log2norm, int64_t* fail, int32_t robust, int32_t mode, void* ws,
+                         size_t ws_bytes, void* stream);
+
+/* Same, but asynchronous: returns 0 once every kernel is enqueued (or a
+ * negative error); the failure count is left in the workspace and read with
+ * hsrq_failure_count (which synchronises the stream). */
+int64_t hsrq_solve_group_async(const double* H, int64_t ldh, int64_t n, int32_t b_r,
+                               const double* lam_re, const double* lam_im, int64_t m_cplx,
+                               int64_t m_real, const double* B, int64_t ldb,
+                               int32_t b_broadcast, double* X, int64_t ldx, double* c_re,
+                               double* c_im, double* s, int64_t ldc, int32_t* seg_exp,
+                               int32_t* alpha_exp, double* norms, double* log2norm,
+                               int64_t* fail, int32_t robust, int32_t mode, void* ws,
+                               size_t ws_bytes, void* stream);
+int64_t hsrq_failure_count(void* ws, void* stream);
+
+/* Kernel launches issued by the last solve on this thread (for accounting). */
+int64_t hsrq_last_launch_count(void);
+
+/* Per-phase device times (ms) of the last solve run with timing enabled:
+ * out_host[0] = diagonal kernels, [1] = panel GEMM kernels, [2] = backtransform,
+ * [3] = setup.  Enable with hsrq_set_timing(1) (adds events, serialises). */
+void hsrq_set_timing(int32_t enable);
+void hsrq_phase_times(double* out_host);
+
+/*
+ * Tile-level entry points (parity tests against the reference kernels).
+ *
+ * hsrq_tile_diag: one diagonal tile, k = rows (<= 128), b shifts.
+ *   hdiag   k x (k-1) row-major (the reference's C-order hdiag tile)
+ *   hleft   k entries (column left of the tile), used iff has_left
+ *   lam_re/lam_im  b shifts (lam_im NULL -> real kernel)
+ *   rright  k x b (real) or k x 2b (complex interleaved) row-major crossover
+ *   x       k x b / k x 2b row-major, in: right-hand side tile, out: solution
+ *   c_re, c_im, s   out, k x b row-major rotations (c_im may be NULL if real)
+ *   beta_exp  in/out, b exponents (beta *= gamma)
+ *   status    out, b int64 packed status (kind << 42 | row), 0 = ok
+ */
+int64_t hsrq_tile_diag(int32_t k, int32_t b, const double* hdiag, const double* hleft,
+                       int32_t has_left, const double* lam_re, const double* lam_im,
+                       const double* rright, double* x, double* c_re, double* c_im, double* s,
+                       int32_t* beta_exp, int64_t* status, int32_t robust, double omega,
+                       void* stream);
+
+/* Elementwise device evaluations for bit-level parity of the scalar helpers. */
+int64_t hsrq_protect_update_batch(const double* bnorm, const double* hnorm, const double* xnorm,
+                                  double omega, int64_t count, double* out, void* stream);
+int64_t hsrq_hypot_batch(const double* x, const double* y, int64_t count, double* out,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSRQ_B200_H */

@@ -1,0 +1,55 @@
+"""In-tree build of libhsrq_b200.so (sm_100a) with nvcc.
+
+The .so is written next to the sources (git-ignored, but it travels to the GPU
+box with the gpurun snapshot).  -fmad=false: the diagonal kernels and the
+panel epilogue reproduce the reference's un-contracted scalar arithmetic
+(_kernels/numba_backend.py:1-7); the tensor-core GEMM is unaffected.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libhsrq_b200.so")
+SOURCES = [os.path.join(CSRC, "hsrq_kernels.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, "hsrq_device.cuh"), os.path.join(ROOT, "include", "hsrq.h")]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+
+def nvcc():
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: cannot build libhsrq_b200.so")
+
+
+def stale():
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(d) > t for d in DEPS)
+
+
+def build(force=False, verbose=False):
+    if not force and not stale():
+        return LIB
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *SOURCES]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.check_call(cmd)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose=True))

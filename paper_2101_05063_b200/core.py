@@ -1,0 +1,118 @@
+"""Types and errors of the reference's solver surface (hessrq core.py), as
+the B200 path consumes and returns them.
+
+Only what the inverse-iteration seam needs: the matrix wrapper (core.py:60-102),
+the tile grid (:105-129), the scaling matrix / solution block (:234-260) and
+the error hierarchy (:39-57), with the same names and semantics so existing
+callers catch the same exceptions.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+class HessrqError(Exception):
+    """Base class for numerical / structural failures (core.py:39-40)."""
+
+
+class ConfigError(HessrqError):
+    """Invalid configuration (core.py:43-44)."""
+
+
+class SingularSystemError(HessrqError):
+    """An exactly singular triangular factor was met (core.py:47-53)."""
+
+    def __init__(self, message, shift_index=None, local_index=None):
+        super().__init__(message)
+        self.shift_index = shift_index
+        self.local_index = local_index
+
+
+class StructuralViolationError(HessrqError):
+    """Input violates the unreduced-Hessenberg structure (core.py:56-57)."""
+
+
+class HessenbergMatrix:
+    """Read-only real upper Hessenberg matrix (core.py:60-98 semantics)."""
+
+    def __init__(self, data):
+        a = np.array(data, dtype=np.float64, order="F")
+        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+            raise ConfigError(f"expected a square matrix, got shape {a.shape}")
+        n = a.shape[0]
+        if n >= 3 and np.any(np.tril(a, -2) != 0.0):
+            raise ConfigError("matrix has nonzeros below the first subdiagonal")
+        a.setflags(write=False)
+        self.n = n
+        self.data = a
+        self._norm_inf = None
+        self._device = {}
+
+    def infinity_norm(self):
+        if self._norm_inf is None:
+            self._norm_inf = float(np.max(np.sum(np.abs(self.data), axis=1)))
+        return self._norm_inf
+
+    def is_unreduced(self):
+        if self.n == 1:
+            return True
+        return bool(np.all(np.diagonal(self.data, -1) != 0.0))
+
+    def __repr__(self):
+        return f"HessenbergMatrix(n={self.n})"
+
+
+def as_hessenberg(h):
+    return h if isinstance(h, HessenbergMatrix) else HessenbergMatrix(h)
+
+
+class TileGrid:
+    """Row/column partition into b_r tiles, last one possibly short (core.py:105-129)."""
+
+    def __init__(self, n, b_r):
+        if not (1 <= b_r <= n):
+            raise ConfigError(f"tile size b_r={b_r} out of range for n={n}")
+        self.n = n
+        self.b_r = b_r
+        self.ranges = [(s, min(s + b_r, n)) for s in range(0, n, b_r)]
+        self.N = len(self.ranges)
+
+    @property
+    def tile_ends(self):
+        return np.array([e for _s, e in self.ranges], dtype=np.int64)
+
+
+@dataclass
+class ScalingMatrix:
+    """Segment scales alpha(tile, shift) = 2**exponent (core.py:234-248)."""
+
+    alpha: np.ndarray
+    exponent: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.alpha = np.asarray(self.alpha, dtype=np.float64)
+
+    def all_ones(self):
+        return bool(np.all(self.alpha == 1.0))
+
+
+@dataclass
+class SolutionBlock:
+    """Solutions plus per-column scales and represented norms (core.py:251-260).
+
+    Extra fields of the B200 path: ``alpha_exp`` / ``log2_norms`` keep the
+    exact exponent and the log2 norm where the reference's doubles would
+    underflow to 0 or overflow to inf.
+    """
+
+    x: np.ndarray
+    alpha: np.ndarray
+    segment_scales: ScalingMatrix | None = None
+    norms: np.ndarray | None = None
+    converged: np.ndarray | None = None
+    flops: dict = field(default_factory=dict)
+    alpha_exp: np.ndarray | None = None
+    log2_norms: np.ndarray | None = None

@@ -1,0 +1,156 @@
+// hsrq_device.cuh -- scalar device arithmetic shared by the kernels.
+//
+// Everything here is written so that, compiled with -fmad=false (no FMA
+// contraction, matching numba's LLVM output, _kernels/numba_backend.py:1-7),
+// it reproduces the reference's scalar arithmetic bit for bit:
+//   * ghypot: glibc 2.39's hypot (the libm routine numba's math.hypot binds,
+//     numba/cpython/mathimpl.py hypot_float_impl), i.e. the non-FMA kernel of
+//     sysdeps/ieee754/dbl-64/e_hypot.c (Borges' algorithm).  CUDA's own hypot
+//     differs by an ulp on ~0.03 % of inputs, which would perturb rotations.
+//   * pow2floor / protect_update: numba_backend.py:37-67, with the result
+//     carried as a log2 exponent.
+//   * complex ops: numba's lowering ((a+bi)(c+di) = (ac-bd)+(ad+bc)i, reals
+//     promoted to (x, 0), CPython's _Py_c_quot division, abs = hypot).
+#pragma once
+#include <cstdint>
+
+namespace hsrq {
+
+constexpr int EXP_ZERO = -1075;  // exponent of a scale that halved to 0
+
+struct cplx {
+  double re, im;
+};
+
+__device__ __forceinline__ cplx mk(double re, double im) { return cplx{re, im}; }
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  double ac = a.re * b.re, bd = a.im * b.im, ad = a.re * b.im, bc = a.im * b.re;
+  return cplx{ac - bd, ad + bc};
+}
+__device__ __forceinline__ cplx csub(cplx a, cplx b) { return cplx{a.re - b.re, a.im - b.im}; }
+__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cplx{a.re + b.re, a.im + b.im}; }
+
+// Exact 2^e for e in [-1075, 1023] (0 below -1074).
+__device__ __forceinline__ double p2(int e) {
+  if (e >= -1022) return __longlong_as_double((long long)(e + 1023) << 52);
+  if (e >= -1074) return __longlong_as_double(1LL << (e + 1074));
+  return 0.0;
+}
+
+// glibc 2.39 e_hypot.c kernel (no __FP_FAST_FMA on x86_64).
+__device__ __forceinline__ double hypot_kernel(double ax, double ay) {
+  double t1, t2;
+  double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+  if (h <= 2.0 * ay) {
+    double delta = h - ay;
+    t1 = ax * (2.0 * delta - ax);
+    t2 = (delta - 2.0 * (ax - ay)) * delta;
+  } else {
+    double delta = h - ax;
+    t1 = 2.0 * delta * (ax - 2.0 * ay);
+    t2 = (4.0 * delta - ay) * ay + delta * delta;
+  }
+  h -= (t1 + t2) / (2.0 * h);
+  return h;
+}
+
+__device__ __noinline__ double ghypot(double x, double y) {
+  if (!isfinite(x) || !isfinite(y)) {
+    if (isinf(x) || isinf(y)) return __longlong_as_double(0x7ff0000000000000LL);
+    return x + y;
+  }
+  x = fabs(x);
+  y = fabs(y);
+  double ax = x < y ? y : x;
+  double ay = x < y ? x : y;
+  if (ax > 0x1p+511) {
+    if (ay <= ax * 0x1p-54) return ax + ay;
+    return hypot_kernel(ax * 0x1p-600, ay * 0x1p-600) / 0x1p-600;
+  }
+  if (ay < 0x1p-511) {
+    if (ax >= ay / 0x1p-54) return ax + ay;
+    return hypot_kernel(ax / 0x1p-600, ay / 0x1p-600) * 0x1p-600;
+  }
+  if (ay <= ax * 0x1p-54) return ax + ay;
+  return hypot_kernel(ax, ay);
+}
+
+__device__ __forceinline__ double cabs_(cplx a) { return ghypot(a.re, a.im); }
+
+// CPython _Py_c_quot as lowered by numba (numba/cpython/numbers.py).
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+  double areal = a.re, aimag = a.im, breal = b.re, bimag = b.im;
+  if (fabs(breal) >= fabs(bimag)) {
+    if (breal == 0.0) return cplx{__longlong_as_double(0x7ff8000000000000LL),
+                                  __longlong_as_double(0x7ff8000000000000LL)};
+    double ratio = bimag / breal;
+    double denom = breal + bimag * ratio;
+    return cplx{(areal + aimag * ratio) / denom, (aimag - areal * ratio) / denom};
+  }
+  double ratio = breal / bimag;
+  double denom = breal * ratio + bimag;
+  return cplx{(areal * ratio + aimag) / denom, (aimag * ratio - areal) / denom};
+}
+
+// pow2floor (numba_backend.py:37-44) as an exponent.
+__device__ __forceinline__ int pow2floor_e(double x) {
+  if (x <= 0.0 || x != x) return -1074;
+  if (isinf(x)) return 0;
+  int e;
+  frexp(x, &e);
+  return e - 1;
+}
+
+// protect_update (numba_backend.py:47-67); returns log2(xi): 0 when xi == 1,
+// EXP_ZERO when the halving loop reached 0.
+__device__ __noinline__ int protect_update_e(double bnorm, double hnorm, double xnorm,
+                                             double omega) {
+  double cand;
+  if (xnorm <= 1.0) {
+    if (bnorm + hnorm * xnorm <= omega) return 0;
+    cand = (omega * 0.5) / (bnorm * 0.5 + (hnorm * xnorm) * 0.5);
+  } else {
+    if (bnorm <= omega && hnorm <= (omega - bnorm) / xnorm) return 0;
+    double u = bnorm / xnorm;
+    cand = ((omega * 0.5) / (u * 0.5 + hnorm * 0.5)) / xnorm;
+  }
+  if (!(cand > 0.0)) cand = 0x1p-1074;
+  if (cand > 1.0) cand = 1.0;
+  int e = pow2floor_e(cand);
+  double xi = p2(e);
+  for (int it = 0; it < 200; it++) {
+    if (xi * bnorm + hnorm * (xi * xnorm) <= omega) break;
+    xi *= 0.5;
+    e -= 1;
+  }
+  if (xi == 0.0) e = EXP_ZERO;
+  return e;
+}
+
+// Cheap test "protect_update would return 1" from upper bounds of the norms;
+// protect_update is monotone in each argument (overflow.py:50-57), so a pass
+// here is exact.  A fail means "evaluate the exact norms".
+__device__ __forceinline__ bool protect_update_is_one(double bnorm, double hnorm, double xnorm,
+                                                      double omega) {
+  if (xnorm <= 1.0) return bnorm + hnorm * xnorm <= omega;
+  return bnorm <= omega && hnorm <= (omega - bnorm) / xnorm;
+}
+
+// Max of non-negative doubles across a warp (NaN never wins, matching the
+// reference's `if abs(v) > vmax` scans).
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// Non-negative double <-> ordered uint64 for atomicMax reductions.
+__device__ __forceinline__ unsigned long long dkey(double v) {
+  return (unsigned long long)__double_as_longlong(v);
+}
+__device__ __forceinline__ double dval(unsigned long long k) { return __longlong_as_double((long long)k); }
+
+}  // namespace hsrq

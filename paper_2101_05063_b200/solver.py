@@ -1,0 +1,244 @@
+"""The GPU seam: one call of libhsrq_b200 per solve group.
+
+Replaces hessrq's ``_solve_group`` (inviter.py:91-106) and the engine of
+``dhsrq3``/``chsrq3`` (backsolve.py:350-388).  PyTorch supplies device memory
+and the stream; all arithmetic runs in the CUDA kernels of csrc/.  A solve
+group may mix real and complex shifts: the kernels place complex shifts
+first (two real columns each) and real shifts after (include/hsrq.h).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import (
+    ConfigError,
+    HessenbergMatrix,
+    ScalingMatrix,
+    SingularSystemError,
+    SolutionBlock,
+    StructuralViolationError,
+)
+
+MAX_TILE = 128  # b_r limit of the GPU path (one warp holds a tile column)
+_KIND_DEGENERATE = 1
+_KIND_SINGULAR = 2
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def default_device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("the hsrq B200 path needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class DeviceHessenberg:
+    """H resident in HBM, column-major with an even leading dimension."""
+
+    def __init__(self, h, device=None):
+        hm = h if isinstance(h, HessenbergMatrix) else HessenbergMatrix(h)
+        self.n = hm.n
+        self.device = device or default_device()
+        self.ldh = self.n + (self.n & 1)
+        t = torch.zeros((self.n, self.ldh), dtype=torch.float64)
+        # row j of t = column j of H (column-major storage)
+        t[:, : self.n] = torch.from_numpy(np.ascontiguousarray(hm.data.T))
+        self.t = t.to(self.device, non_blocking=False)
+
+    @classmethod
+    def of(cls, h, device=None):
+        """Cached device copy attached to a HessenbergMatrix."""
+        hm = h if isinstance(h, HessenbergMatrix) else HessenbergMatrix(h)
+        dev = device or default_device()
+        key = str(dev)
+        d = hm._device.get(key)
+        if d is None:
+            d = cls(hm, dev)
+            hm._device[key] = d
+        return d
+
+
+@dataclass
+class GroupOutput:
+    """Device-side results of one solve group (torch tensors)."""
+
+    X: torch.Tensor          # (ncol, n): row c = column c
+    c_re: torch.Tensor       # (ms, n)
+    c_im: torch.Tensor
+    s: torch.Tensor
+    seg_exp: torch.Tensor    # (N, ms) int32
+    alpha_exp: torch.Tensor  # (ms,) int32
+    norms: torch.Tensor
+    log2norm: torch.Tensor
+    fail: torch.Tensor       # (ms,) int64
+    nfail: int
+    mc: int
+    mr: int
+    launches: int
+
+
+class GroupSolver:
+    """Device buffers for one (n, b_r, m_cplx, m_real) shape, reusable across calls."""
+
+    def __init__(self, dh: DeviceHessenberg, b_r, m_cplx, m_real):
+        if not (1 <= b_r <= dh.n):
+            raise ConfigError(f"tile size b_r={b_r} out of range for n={dh.n}")
+        if b_r > MAX_TILE:
+            raise ConfigError(f"the B200 path supports b_r <= {MAX_TILE} (got {b_r})")
+        self.lib = _lib.load()
+        self.dh = dh
+        self.n, self.b_r = dh.n, int(b_r)
+        self.N = (self.n + self.b_r - 1) // self.b_r
+        self.mc, self.mr = int(m_cplx), int(m_real)
+        self.ms = self.mc + self.mr
+        self.ncol = 2 * self.mc + self.mr
+        dev = dh.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.X = torch.empty((self.ncol, self.n), **f64)
+        self.c_re = torch.empty((self.ms, self.n), **f64)
+        self.c_im = torch.empty((self.ms, self.n), **f64)
+        self.s = torch.empty((self.ms, self.n), **f64)
+        self.seg_exp = torch.empty((self.N, self.ms), dtype=torch.int32, device=dev)
+        self.alpha_exp = torch.empty(self.ms, dtype=torch.int32, device=dev)
+        self.norms = torch.empty(self.ms, **f64)
+        self.log2norm = torch.empty(self.ms, **f64)
+        self.fail = torch.empty(self.ms, dtype=torch.int64, device=dev)
+        self.lam_re = torch.empty(self.ms, **f64)
+        self.lam_im = torch.empty(self.ms, **f64)
+        self.ws_bytes = int(self.lib.hsrq_workspace_bytes(self.n, self.b_r, self.mc, self.mr))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+
+    def set_shifts(self, lam_cplx, lam_real):
+        lam = np.concatenate([np.asarray(lam_cplx, dtype=np.complex128).ravel(),
+                              np.asarray(lam_real, dtype=np.float64).ravel().astype(np.complex128)])
+        self.lam_re.copy_(torch.from_numpy(np.ascontiguousarray(lam.real)))
+        self.lam_im.copy_(torch.from_numpy(np.ascontiguousarray(lam.imag)))
+
+    def launch(self, B, broadcast, robust=True, mode="eigvec", stream=None, sync=True):
+        """Enqueue the whole sweep.  B: device (n,) vector (broadcast) or (ncol, n)."""
+        stream = stream or torch.cuda.current_stream(self.dh.device)
+        mode_i = {"solve": 0, "eigvec": 1}[mode]
+        args = (
+            _ptr(self.dh.t), self.dh.ldh, self.n, self.b_r, _ptr(self.lam_re), _ptr(self.lam_im),
+            self.mc, self.mr, _ptr(B), 0 if broadcast else self.n, 1 if broadcast else 0,
+            _ptr(self.X), self.n, _ptr(self.c_re), _ptr(self.c_im), _ptr(self.s), self.n,
+            _ptr(self.seg_exp), _ptr(self.alpha_exp), _ptr(self.norms), _ptr(self.log2norm),
+            _ptr(self.fail), int(bool(robust)), mode_i, _ptr(self.ws), self.ws_bytes,
+            ctypes.c_void_p(stream.cuda_stream),
+        )
+        fn = self.lib.hsrq_solve_group if sync else self.lib.hsrq_solve_group_async
+        r = fn(*args)
+        if r < 0:
+            raise RuntimeError(f"hsrq_solve_group failed ({r}): {_lib.last_error()}")
+        return int(r)
+
+    def output(self, nfail):
+        return GroupOutput(self.X, self.c_re, self.c_im, self.s, self.seg_exp, self.alpha_exp,
+                           self.norms, self.log2norm, self.fail, nfail, self.mc, self.mr,
+                           int(self.lib.hsrq_last_launch_count()))
+
+
+def _check_h(hm):
+    if not hm.is_unreduced():
+        raise ConfigError("matrix must be unreduced (nonzero subdiagonal)")
+
+
+def raise_first_failure(fail_codes, b_c, kinds):
+    """Raise the exception the reference would raise first.
+
+    ``fail_codes`` per shift of one solve call (inviter/backsolve call order),
+    ``kinds`` a list of (start, stop) shift ranges, each one reference call
+    (its own batches).  Reference order: every reduction precedes every solve
+    (tiled_reduce runs before _substitute), batches in order, tile columns
+    right to left, rows bottom-up within a kernel, then the batch-local shift
+    (scheduler.py:189-219, numba_backend.py:79-106, 138-192).
+    """
+    codes = np.asarray(fail_codes, dtype=np.int64)
+    best = None
+    for call_i, (lo, hi) in enumerate(kinds):
+        sub = codes[lo:hi]
+        bad = np.nonzero(sub)[0]
+        if bad.size == 0:
+            continue
+        for phase in (_KIND_DEGENERATE, _KIND_SINGULAR):
+            cands = []
+            for q in bad:
+                code = int(sub[q])
+                ph, tile, row = code >> 56, (code >> 24) & 0xFFFFFFFF, code & 0xFFFFFF
+                if ph != phase:
+                    continue
+                bc = max(1, min(b_c, hi - lo))
+                cands.append(((q // bc), -tile, -row, q % bc, q, tile, row))
+            if cands:
+                best = (phase,) + min(cands)
+                break
+        if best is not None:
+            break
+    if best is None:
+        return
+    phase, _b, _t, _r, _l, q, tile, row = best
+    if phase == _KIND_DEGENERATE:
+        raise StructuralViolationError(
+            f"degenerate rotation in tile column {tile} at local row {row}, "
+            f"shift {q} (both pivot entries are zero)")
+    raise SingularSystemError(
+        f"singular triangular factor for shift {q} (local row {row})",
+        shift_index=int(q), local_index=int(row))
+
+
+def solve_group(h, eigs_cplx, eigs_real, b, b_r, *, robust=True, mode="eigvec", b_c=32,
+                device=None, solver=None):
+    """Run one solve group; returns (GroupOutput, GroupSolver).
+
+    ``b``: a real n-vector used for every column (the inverse-iteration
+    start vector) or a host/device matrix (n, ncol) in the column layout.
+    """
+    hm = h if isinstance(h, HessenbergMatrix) else HessenbergMatrix(h)
+    _check_h(hm)
+    dh = DeviceHessenberg.of(hm, device)
+    mc = len(np.atleast_1d(eigs_cplx)) if eigs_cplx is not None else 0
+    mr = len(np.atleast_1d(eigs_real)) if eigs_real is not None else 0
+    gs = solver or GroupSolver(dh, b_r, mc, mr)
+    gs.set_shifts(eigs_cplx if mc else [], eigs_real if mr else [])
+    bt = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64))
+    broadcast = bt.dim() == 1
+    if not broadcast:
+        bt = bt.T.contiguous() if bt.shape[0] == hm.n and bt.shape[1] == gs.ncol else bt
+    bt = bt.to(dh.device)
+    nfail = gs.launch(bt, broadcast, robust=robust, mode=mode)
+    return gs.output(nfail), gs
+
+
+def to_solution_block(out: GroupOutput, n, *, robust=True, want_cplx):
+    """Host SolutionBlock in the reference's layout for a single-kind group."""
+    X = out.X.cpu().numpy()
+    if want_cplx:
+        x = (X[0 : 2 * out.mc : 2] + 1j * X[1 : 2 * out.mc : 2]).T.copy()
+    else:
+        x = X[2 * out.mc :].T.copy()
+    sl = slice(0, out.mc) if want_cplx else slice(out.mc, out.mc + out.mr)
+    seg = out.seg_exp.cpu().numpy()[:, sl].copy()
+    aexp = out.alpha_exp.cpu().numpy()[sl].copy()
+    norms = out.norms.cpu().numpy()[sl].copy()
+    l2 = out.log2norm.cpu().numpy()[sl].copy()
+    if not robust:
+        return SolutionBlock(x=x, alpha=np.ones(aexp.size),
+                             segment_scales=ScalingMatrix(np.ones(seg.shape), np.zeros_like(seg)),
+                             norms=None, alpha_exp=np.zeros_like(aexp))
+    return SolutionBlock(x=x, alpha=np.ldexp(1.0, aexp),
+                         segment_scales=ScalingMatrix(np.ldexp(1.0, seg), seg), norms=norms,
+                         alpha_exp=aexp, log2_norms=l2)
+
+
+def converged_log2(log2_norm, n):
+    """``converged`` (inviter.py:71-73) evaluated on log2 of the represented norm."""
+    return log2_norm > math.log2(0.1 / math.sqrt(n))

@@ -1,0 +1,87 @@
+"""The CPU oracle is pinned to the live reference's outputs (tests/golden,
+made by tools/make_golden.py from hessrq's numba backend)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+
+def test_hypot_matches_glibc_fixture():
+    import ctypes
+
+    g = golden("scalars")
+    libm = ctypes.CDLL("libm.so.6")
+    libm.hypot.restype = ctypes.c_double
+    libm.hypot.argtypes = [ctypes.c_double, ctypes.c_double]
+    out = np.array([libm.hypot(a, b) for a, b in zip(g["hx"], g["hy"])])
+    assert np.array_equal(out, g["hypot"])
+
+
+def test_protect_update_and_pow2floor(oracle):
+    g = golden("scalars")
+    om = float(g["omega"])
+    out = np.array([oracle.protect_update(a, b, c, om) for a, b, c in zip(g["pb"], g["ph"], g["px"])])
+    assert np.array_equal(out, g["protect"])
+    assert np.array_equal(np.array([oracle.pow2floor(v) for v in g["p2in"]]), g["p2out"])
+
+
+def test_tile_kernels_bitwise(oracle):
+    g = golden("tiles")
+    for t in range(int(g["ntiles"])):
+        k, b, has_left, st_r, st_s, st_cr, st_cs = (int(v) for v in g[f"t{t}_meta"])
+        om = float(g[f"t{t}_omega"])
+        hd, hl = g[f"t{t}_hdiag"], g[f"t{t}_hleft"]
+        st, c, s = oracle.reduce_diag(hd, hl, has_left, g[f"t{t}_lam"], g[f"t{t}_rright"])
+        assert st == st_r
+        assert np.array_equal(c, g[f"t{t}_c"]) and np.array_equal(s, g[f"t{t}_s"])
+        st, x, be = oracle.solve_rsolve(hd, hl, has_left, g[f"t{t}_lam"], g[f"t{t}_rright"], c, s,
+                                        g[f"t{t}_xin"], np.zeros(b), True, om)
+        assert st == st_s
+        assert np.array_equal(x, g[f"t{t}_x"])
+        assert np.array_equal(np.ldexp(1.0, be), g[f"t{t}_beta"])
+        st, cre, cim, cs = oracle.creduce_diag(hd, hl, has_left, g[f"t{t}_clr"], g[f"t{t}_cli"],
+                                               g[f"t{t}_rr2"])
+        assert st == st_cr
+        assert np.array_equal(cre, g[f"t{t}_cre"]) and np.array_equal(cim, g[f"t{t}_cim"])
+        assert np.array_equal(cs, g[f"t{t}_cs"])
+        st, x2, be = oracle.csolve_crsolve(hd, hl, has_left, g[f"t{t}_clr"], g[f"t{t}_cli"],
+                                           g[f"t{t}_rr2"], cre, cim, cs, g[f"t{t}_x2in"],
+                                           np.zeros(b), True, om)
+        assert st == st_cs
+        assert np.array_equal(x2, g[f"t{t}_x2"])
+        assert np.array_equal(np.ldexp(1.0, be), g[f"t{t}_cbeta"])
+
+
+def test_full_solves(oracle, same_blas):
+    """dhsrq3/chsrq3 end to end: bitwise when the BLAS kernel family matches."""
+    g = golden("solves")
+    for tag in g["tags"]:
+        b_r, b_c, robust, mode, cplx = (int(v) for v in g[f"{tag}_cfg"])
+        r = oracle.solve(g[f"{tag}_h"], g[f"{tag}_lam"], g[f"{tag}_b"], b_r, b_c, robust=bool(robust),
+                         mode=("solve", "eigvec")[mode])
+        xr = g[f"{tag}_x"]
+        if robust:
+            assert np.array_equal(r.segment_scales, g[f"{tag}_seg"]), tag
+            assert np.array_equal(r.alpha, g[f"{tag}_alpha"]), tag
+        if same_blas:
+            assert np.array_equal(r.x, xr), tag
+            if robust:
+                assert np.array_equal(r.norms, g[f"{tag}_norms"]), tag
+        else:
+            scale = np.max(np.abs(xr)) or 1.0
+            assert np.max(np.abs(r.x - xr)) <= 1e-12 * scale, tag
+
+
+def test_restart_stream():
+    from paper_2101_05063_b200 import rng
+    from paper_2101_05063_b200.inviter import _next_start
+
+    g = golden("scalars")
+    for s, row in zip(g["seeds"], g["uoc"]):
+        assert np.array_equal(rng.uniform_open_closed(int(s), 64), row)
+    prev = [1e-14 * np.ones(37)]
+    for att, want in zip((1, 2, 3), g["starts"]):
+        v = _next_start(1e-14, 37, prev, 0x5EED, att)
+        prev.append(v.copy())
+        assert np.array_equal(v, want)

@@ -1,0 +1,221 @@
+"""Generate tests/golden/*.npz from the LIVE reference (hessrq, numba backend).
+
+Run in the build container, where /root/reference exists:
+    python tools/make_golden.py
+The fixtures pin the CPU oracle (oracle/) and the GPU path to the reference's
+own outputs: tile kernels, scalar helpers, full dhsrq3/chsrq3 solves (robust,
+non-robust, solve/eigvec modes, ragged tiles, the H2 overflow fixture of
+verifysuite.py:107-124), the inverse-iteration drivers and BASELINE config 1.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "tests", "golden")
+sys.path.insert(0, REF)
+sys.path.insert(0, ROOT)
+
+import hessrq  # noqa: E402
+from hessrq import _kernels  # noqa: E402
+from hessrq.backsolve import chsrq3, dhsrq3  # noqa: E402
+from hessrq.inviter import InviterConfig, _next_start, chsrq3in, dhsrq3in, hsrq3in  # noqa: E402
+from hessrq.testprob import gen_h1, gen_h2, gen_h3, uniform_open_closed  # noqa: E402
+from hessrq.verifysuite import random_unreduced  # noqa: E402
+
+assert hessrq.backend_name() == "numba", "numba backend required (see SURVEY.md §0 finding 5)"
+K = _kernels.get_backend()
+_DMAX = float(np.finfo(np.float64).max)
+
+
+def blas_corename():
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+
+    return O.blas_corename()
+
+
+def save(name, **arrs):
+    os.makedirs(OUT, exist_ok=True)
+    arrs["corename"] = np.array(blas_corename())
+    np.savez_compressed(os.path.join(OUT, name + ".npz"), **arrs)
+
+
+def gen_scalars():
+    rng = np.random.default_rng(7)
+    libm = ctypes.CDLL("libm.so.6")
+    libm.hypot.restype = ctypes.c_double
+    libm.hypot.argtypes = [ctypes.c_double, ctypes.c_double]
+    e1 = rng.integers(-1070, 1020, 4000)
+    e2 = np.clip(e1 + rng.integers(-60, 60, 4000), -1074, 1023)
+    hx = rng.uniform(-1, 1, 4000) * np.ldexp(1.0, e1)
+    hy = rng.uniform(-1, 1, 4000) * np.ldexp(1.0, e2)
+    hx[:8] = [0.0, 3.0, 1e308, 5e-324, -0.0, 1.0, 2.0 ** 511, 2.0 ** -511]
+    hy[:8] = [0.0, 4.0, 1e308, 5e-324, 7.0, 1e-20, 3.0, 2.0 ** -600]
+    hyp = np.array([libm.hypot(a, b) for a, b in zip(hx, hy)])
+    omega = _DMAX / 2.0 / 128
+    pb = np.abs(rng.standard_normal(3000)) * np.ldexp(1.0, rng.integers(-20, 1024, 3000))
+    ph = np.abs(rng.standard_normal(3000)) * np.ldexp(1.0, rng.integers(-20, 600, 3000))
+    px = np.abs(rng.standard_normal(3000)) * np.ldexp(1.0, rng.integers(-300, 700, 3000))
+    pb = np.where(np.isfinite(pb), pb, 1e300)
+    pu = np.array([K.protect_update(a, b, c, omega) for a, b, c in zip(pb, ph, px)])
+    f2 = np.abs(rng.standard_normal(500)) * np.ldexp(1.0, rng.integers(-1074, 1000, 500))
+    f2[:4] = [0.0, -1.0, np.inf, 5e-324]
+    p2f = np.array([K.pow2floor(v) for v in f2])
+    seeds = np.array([0x5EED, 0x5EED + 0x9E37, 12345, 2**63 + 17], dtype=np.uint64)
+    uoc = np.stack([uniform_open_closed(int(s), 64) for s in seeds])
+    # restart vectors, inviter.py:76-88
+    n = 37
+    rho = 1e-14
+    prev = [rho * np.ones(n)]
+    starts = []
+    for att in (1, 2, 3):
+        v = _next_start(rho, n, prev, 0x5EED, att)
+        prev.append(v.copy())
+        starts.append(v)
+    save("scalars", hx=hx, hy=hy, hypot=hyp, pb=pb, ph=ph, px=px, omega=np.float64(omega),
+         protect=pu, p2in=f2, p2out=p2f, seeds=seeds, uoc=uoc, starts=np.stack(starts))
+
+
+def gen_tiles():
+    rng = np.random.default_rng(11)
+    cases = {}
+    idx = 0
+    for k, b, has_left, small_omega in ((16, 3, True, False), (37, 4, False, False),
+                                        (128, 3, True, False), (64, 5, True, True),
+                                        (128, 2, False, True), (1, 2, True, False),
+                                        (2, 3, False, False)):
+        h = random_unreduced(max(k, 2) + 1, 100 + idx).data
+        hdiag = np.ascontiguousarray(h[1 : k + 1, 1:k])
+        hleft = np.ascontiguousarray(h[1 : k + 1, 0])
+        lam = rng.uniform(-3, 3, b)
+        rright = rng.standard_normal((k, b))
+        xin = rng.standard_normal((k, b)) * (1e300 if small_omega else 1.0)
+        omega = 1e10 if small_omega else _DMAX / 2.0 / 128
+        c = np.empty((k, b))
+        s = np.empty((k, b))
+        st_r = K.reduce_diag(hdiag, hleft, has_left, lam, rright, c, s)
+        x = xin.copy()
+        beta = np.ones(b)
+        st_s = K.solve_rsolve(hdiag, hleft, has_left, lam, rright, c, s, x, beta, True, omega)
+        # complex
+        clr, cli = rng.uniform(-3, 3, b), rng.uniform(0.1, 3, b)
+        rr2 = rng.standard_normal((k, 2 * b))
+        x2in = rng.standard_normal((k, 2 * b)) * (1e300 if small_omega else 1.0)
+        cre, cim, cs = np.empty((k, b)), np.empty((k, b)), np.empty((k, b))
+        st_cr = K.creduce_diag(hdiag, hleft, has_left, clr, cli, rr2, cre, cim, cs)
+        x2 = x2in.copy()
+        cbeta = np.ones(b)
+        st_cs = K.csolve_crsolve(hdiag, hleft, has_left, clr, cli, rr2, cre, cim, cs, x2, cbeta,
+                                 True, omega)
+        cases.update({
+            f"t{idx}_meta": np.array([k, b, int(has_left), int(st_r), int(st_s), int(st_cr),
+                                      int(st_cs)], dtype=np.int64),
+            f"t{idx}_omega": np.float64(omega),
+            f"t{idx}_hdiag": hdiag, f"t{idx}_hleft": hleft, f"t{idx}_lam": lam,
+            f"t{idx}_rright": rright, f"t{idx}_xin": xin, f"t{idx}_c": c, f"t{idx}_s": s,
+            f"t{idx}_x": x, f"t{idx}_beta": beta, f"t{idx}_clr": clr, f"t{idx}_cli": cli,
+            f"t{idx}_rr2": rr2, f"t{idx}_x2in": x2in, f"t{idx}_cre": cre, f"t{idx}_cim": cim,
+            f"t{idx}_cs": cs, f"t{idx}_x2": x2, f"t{idx}_cbeta": cbeta,
+        })
+        idx += 1
+    save("tiles", ntiles=np.int64(idx), **cases)
+
+
+def _solve_case(store, tag, h, lam, b, b_r, b_c, robust, mode, cplx):
+    f = chsrq3 if cplx else dhsrq3
+    r = f(h, lam, b, b_r=b_r, b_c=b_c, robust=robust, mode=mode)
+    store[f"{tag}_h"] = np.asfortranarray(h.data if hasattr(h, "data") else h)
+    store[f"{tag}_lam"] = lam
+    store[f"{tag}_b"] = b
+    store[f"{tag}_cfg"] = np.array([b_r, b_c, int(robust), {"solve": 0, "eigvec": 1}[mode],
+                                    int(cplx)], dtype=np.int64)
+    store[f"{tag}_x"] = r.x
+    store[f"{tag}_alpha"] = r.alpha
+    store[f"{tag}_seg"] = r.segment_scales.alpha
+    store[f"{tag}_norms"] = r.norms if r.norms is not None else np.full(len(lam), np.nan)
+
+
+def gen_solves():
+    store = {}
+    tags = []
+    rng = np.random.default_rng(3)
+    specs = [(24, 6, 2, 1), (70, 16, 5, 2), (64, 64, 3, 3), (33, 8, 32, 4), (129, 32, 7, 5),
+             (200, 128, 16, 6), (40, 5, 1, 7)]
+    for n, b_r, b_c, seed in specs:
+        h = random_unreduced(n, seed)
+        nrm = h.infinity_norm()
+        lam = nrm * rng.uniform(-2, 2, 6)
+        b = rng.standard_normal((n, 6))
+        clam = nrm * (rng.uniform(-2, 2, 4) + 1j * rng.uniform(0.05, 2, 4))
+        cb = rng.standard_normal((n, 4)) + 1j * rng.standard_normal((n, 4))
+        for robust, mode in ((True, "solve"), (True, "eigvec"), (False, "solve")):
+            t = f"s{len(tags)}"
+            _solve_case(store, t, h, lam, b, b_r, b_c, robust, mode, False)
+            tags.append(t)
+            t = f"s{len(tags)}"
+            _solve_case(store, t, h, clam, cb, b_r, b_c, robust, mode, True)
+            tags.append(t)
+    # overflow fixture (verifysuite.py:107-124)
+    for b_r in (16, 7, 60):
+        t = f"s{len(tags)}"
+        _solve_case(store, t, gen_h2(60), np.array([2.0]), 1e290 * np.ones((60, 1)), b_r, 1, True,
+                    "solve", False)
+        tags.append(t)
+    t = f"s{len(tags)}"
+    _solve_case(store, t, gen_h2(60), np.array([2.0 + 0.5j]), 1e290 * np.ones((60, 1)) + 0j, 16,
+                1, True, "solve", True)
+    tags.append(t)
+    t = f"s{len(tags)}"
+    _solve_case(store, t, gen_h3(60), np.array([2.0]), np.ones((60, 1)), 16, 1, True, "solve",
+                False)
+    tags.append(t)
+    save("solves", tags=np.array(tags), **store)
+
+
+def gen_inviter():
+    store = {}
+    # H1 with known eigenvalues, real and complex parts
+    h, eigs = gen_h1(32, 0.5, seed=4)
+    cfg = InviterConfig(b_r=8, b_c=4)
+    r = hsrq3in(h, eigs, cfg)
+    store.update(h1_h=np.asfortranarray(h.data), h1_eigs=eigs, h1_vectors=r.vectors,
+                 h1_conv=r.converged, h1_restarts=r.restarts, h1_norms=r.norms)
+    sel = eigs[eigs.imag > 0]
+    rc = chsrq3in(h, sel.conj(), cfg)
+    store.update(h1c_vectors=rc.vectors, h1c_norms=rc.norms)
+    rr = dhsrq3in(h, eigs[eigs.imag == 0].real, cfg)
+    store.update(h1r_vectors=rr.vectors, h1r_norms=rr.norms, h1r_restarts=rr.restarts)
+    # a case with restarts: shifts exactly at eigenvalues of a tiny matrix + far shift
+    h2 = random_unreduced(20, 5)
+    ev = np.linalg.eigvals(h2.data)
+    shifts = np.concatenate([ev[np.abs(ev.imag) == 0].real[:3], [1e3]])
+    r2 = dhsrq3in(h2, shifts, InviterConfig(b_r=5, b_c=2))
+    store.update(rs_h=np.asfortranarray(h2.data), rs_shifts=shifts, rs_vectors=r2.vectors,
+                 rs_conv=r2.converged, rs_restarts=r2.restarts, rs_norms=r2.norms)
+    # BASELINE config 1 (n=256, all real, b_r=32): dhsrq3in through hsrq3in
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import instances
+
+    h1 = instances.make_h(1)
+    s1 = instances.shifts(1)
+    r1 = hsrq3in(h1, s1, InviterConfig(b_r=32))
+    store.update(c1_h=h1, c1_shifts=s1, c1_vectors=r1.vectors.real, c1_conv=r1.converged,
+                 c1_restarts=r1.restarts, c1_norms=r1.norms)
+    save("inviter", **store)
+
+
+if __name__ == "__main__":
+    gen_scalars()
+    gen_tiles()
+    gen_solves()
+    gen_inviter()
+    for f in sorted(os.listdir(OUT)):
+        print(f, os.path.getsize(os.path.join(OUT, f)))
