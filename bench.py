@@ -1,0 +1,423 @@
+"""Benchmark: eigenvectors/s and fp64 TFLOP/s of the batched shifted-Hessenberg
+robust RQ solve (BASELINE.json metric) on BASELINE config 5.
+
+Workload (config 5): n = 16000 random unreduced Hessenberg (seeded, triu
+N(0,1) + |N(0,1)|+0.1 subdiagonal), every real eigenvalue plus one member of
+every conjugate pair as shifts (3790 real + 6105 complex = 16000 real
+columns), b_r = 128, start vector eps*||H||_inf*ones (inviter.py:117-133).
+A step = one _solve_group attempt over all shifts: the full tiled reduce +
+robust substitution + normalise/backtransform sweep.  Inputs (H 2 GB, X
+2 GB) are far larger than L2 (126 MB), so no explicit flush is needed.
+
+  python bench.py [--gpus N --steps K --warmup W]      our B200 path
+  python bench.py --impl reference ...                 the CPU oracle port
+
+Under torchrun (N > 1) shifts are partitioned by cost over the ranks (H
+replicated), each rank runs its own sweep, and X is gathered to rank 0 with
+NCCL inside the timed step (strong scaling: total work fixed).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "eigenvectors/s and fp64 TFLOP/s (% of peak), n=16000, at 1/2/4/8 B200"
+FP64_PEAK_FALLBACK = 37.1  # TFLOP/s, DMMA m16n8k4 measured on this pool (profiles/fp64_peak_r01.txt)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    d = {}
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+    fp64 = d.get("fp64_tflops")
+    src = "MEASURED_PEAKS.json" if fp64 else "measured (tools/microbench/fp64_peak.cu, profiles/fp64_peak_r01.txt)"
+    return float(fp64 or FP64_PEAK_FALLBACK), src, float(d.get("hbm_gbs", 6469.3))
+
+
+def workload(cfg, seed=0, n_override=None):
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import instances
+
+    n = n_override or {3: 4000, 4: 2000, 5: 16000, 2: 4000, 1: 256}[cfg]
+    h = instances.make_h(cfg, seed, n=n)
+    if n_override:
+        import scipy.linalg as sl
+
+        ev = sl.eigvals(h)
+        sel = ev[ev.imag >= 0]
+    else:
+        sel = instances.shifts(cfg, seed)
+    er = np.sort(sel[sel.imag == 0].real)
+    ec = sel[sel.imag > 0]
+    b_r = {1: 32, 2: 64}.get(cfg, 128)
+    return h, er, ec, b_r
+
+
+def partition(er, ec, rank, world):
+    """Cost-balanced shard: complex ~2.04x a real shift (flop model at n=16000)."""
+    if world == 1:
+        return er, ec
+    wr = np.array_split(er, world)[rank]
+    wc = np.array_split(ec, world)[rank]
+    return wr, wc
+
+
+class ClockSampler:
+    """nvidia-smi style clock/throttle sampling during the timed region (pynvml)."""
+
+    REASONS = {
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index=0, period=0.1):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_sample(h, er, ec, b_r, n_real=16, n_cplx=16, threads=None):
+    """Time the CPU oracle port on a bounded sample of the same workload."""
+    from oracle import oracle as O
+
+    O.build()
+    try:
+        O.use_reference_blas(True)
+    except Exception:
+        pass
+    threads = threads or os.cpu_count() or 1
+    rng = np.random.default_rng(1)
+    sr = er[rng.choice(er.size, min(n_real, er.size), replace=False)] if er.size else er
+    sc = ec[rng.choice(ec.size, min(n_cplx, ec.size), replace=False)] if ec.size else ec
+    n = h.shape[0]
+    rho = np.finfo(float).eps * np.max(np.sum(np.abs(h), axis=1))
+    # one batch per thread (b_c = shifts per thread)
+    t0 = time.perf_counter()
+    if sr.size:
+        bc = max(1, -(-sr.size // threads))
+        O.solve(h, sr, np.repeat(rho * np.ones((n, 1)), sr.size, 1), b_r, bc, mode="eigvec",
+                nthreads=threads)
+    if sc.size:
+        bc = max(1, -(-sc.size // threads))
+        O.solve(h, sc, np.repeat(rho * np.ones((n, 1)), sc.size, 1).astype(complex), b_r, bc,
+                mode="eigvec", nthreads=threads)
+    dt = time.perf_counter() - t0
+    return (sr.size + sc.size), dt, threads, f"{sr.size} real + {sc.size} complex shifts of the same H"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    h, er, ec, b_r = workload(args.config, n_override=args.n)
+    from paper_2101_05063_b200 import flops as F
+
+    nshift, dts = 0, []
+    for i in range(args.warmup + args.steps):
+        cnt, dt, threads, sample = cpu_sample(h, er, ec, b_r, args.cpu_real, args.cpu_cplx)
+        if i >= args.warmup:
+            dts.append(dt)
+            nshift = cnt
+    t = float(np.mean(dts))
+    v = nshift / t
+    n = h.shape[0]
+    fl = F.reference_flops(n, b_r, min(args.cpu_real, er.size), min(args.cpu_cplx, ec.size))
+    line = {
+        "metric": METRIC, "impl": "reference", "value": v, "unit": "eigenvectors/s",
+        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded config-5 instance, LAPACK eigenvalues as shifts)",
+        "config": {"workload": f"config{args.config}: n={n}, b_r={b_r}, bounded CPU sample",
+                   "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "eigenvectors/s", "cores": threads, "kind": "port",
+                         "sample": sample, "tflops": fl / t / 1e12},
+        "e2e": {"value": v, "unit": "eigenvectors/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2101_05063_b200 import _lib
+    from paper_2101_05063_b200 import flops as F
+    from paper_2101_05063_b200.core import HessenbergMatrix
+    from paper_2101_05063_b200.solver import DeviceHessenberg, GroupSolver
+
+    h, er, ec, b_r = workload(args.config, n_override=args.n)
+    n = h.shape[0]
+    m_total_r, m_total_c = er.size, ec.size
+    my_r, my_c = partition(er, ec, rank, world)
+    hm = HessenbergMatrix(h)
+    rho = np.finfo(float).eps * hm.infinity_norm()
+    lib = _lib.load()
+
+    dh = DeviceHessenberg(hm, dev)
+    gs = GroupSolver(dh, b_r, my_c.size, my_r.size)
+    gs.set_shifts(my_c, my_r)
+    start = torch.full((n,), rho, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(timing=False):
+        lib.hsrq_set_timing(1 if timing else 0)
+        r = gs.launch(start, True, robust=True, mode="eigvec", stream=stream, sync=False)
+        return r
+
+    gather_bufs = None
+    if world > 1:
+        cols = [None] * world
+        counts = torch.tensor([gs.ncol], device=dev)
+        allc = [torch.zeros_like(counts) for _ in range(world)]
+        dist.all_gather(allc, counts)
+        maxc = int(max(int(c.item()) for c in allc))
+        gather_bufs = [torch.empty((maxc, n), dtype=torch.float64, device=dev) for _ in range(world)] if rank == 0 else None
+        send = torch.zeros((maxc, n), dtype=torch.float64, device=dev)
+
+    def gather():
+        if world == 1:
+            return
+        send[: gs.ncol].copy_(gs.X)
+        dist.gather(send, gather_bufs if rank == 0 else None, dst=0)
+
+    for _ in range(args.warmup):
+        step()
+        gather()
+    torch.cuda.synchronize()
+    nf = lib.hsrq_failure_count(ctypes.c_void_p(gs.ws.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    phase = np.zeros(4)
+    launches = 0
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(timing=True)
+            launches += int(lib.hsrq_last_launch_count())
+            pt = np.zeros(4)
+            lib.hsrq_phase_times(ctypes.c_void_p(pt.ctypes.data))
+            phase += pt
+            gather()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms = float(t_local.item())
+    phase /= args.steps
+
+    # ---- e2e through the C ABI with host (pinned) buffers ----
+    e2e = None
+    if not args.no_e2e:
+        h_host = torch.empty((n, dh.ldh), dtype=torch.float64).pin_memory()
+        h_host.copy_(dh.t.cpu())
+        x_host = torch.empty((gs.ncol, n), dtype=torch.float64).pin_memory()
+        lam_host = torch.empty(gs.ms, dtype=torch.float64).pin_memory()
+        lam_host.copy_(gs.lam_re.cpu())
+        lam_i_host = torch.empty(gs.ms, dtype=torch.float64).pin_memory()
+        lam_i_host.copy_(gs.lam_im.cpu())
+        aux = torch.empty((4, gs.ms), dtype=torch.float64).pin_memory()
+        h2d = h_host.numel() * 8 + 2 * gs.ms * 8
+        d2h = x_host.numel() * 8 + aux.numel() * 8
+        def e2e_step():
+            dh.t.copy_(h_host, non_blocking=True)
+            gs.lam_re.copy_(lam_host, non_blocking=True)
+            gs.lam_im.copy_(lam_i_host, non_blocking=True)
+            step()
+            gather()
+            x_host.copy_(gs.X, non_blocking=True)
+            aux[0].copy_(gs.norms, non_blocking=True)
+            aux[1].copy_(gs.log2norm, non_blocking=True)
+            aux[2].copy_(gs.alpha_exp.to(torch.float64), non_blocking=True)
+            aux[3].copy_(gs.fail.to(torch.float64), non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ee0 = torch.cuda.Event(enable_timing=True)
+        ee1 = torch.cuda.Event(enable_timing=True)
+        ee0.record(stream)
+        for _ in range(max(1, args.steps)):
+            e2e_step()
+        ee1.record(stream)
+        torch.cuda.synchronize()
+        ems = ee0.elapsed_time(ee1) / max(1, args.steps)
+        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ems = float(te.item())
+        e2e = {"value": (m_total_r + m_total_c) / (ems / 1e3), "unit": "eigenvectors/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": ems}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_src, hbm = load_peaks()
+    nvec = m_total_r + m_total_c
+    ref_fl = F.reference_flops(n, b_r, m_total_r, m_total_c)
+    exe_fl = F.executed_flops(n, b_r, m_total_r, m_total_c)
+    my_ref_fl = F.reference_flops(n, b_r, my_r.size, my_c.size)
+    # panel kernel: algorithmic work = reference ReduceOffdiag + Update flops
+    N = (n + b_r - 1) // b_r
+    pan_alg = my_ref_fl - (my_r.size * (F.per_shift_flops(n, b_r, False) - _offdiag_update(n, b_r, False))
+                           + my_c.size * (F.per_shift_flops(n, b_r, True) - _offdiag_update(n, b_r, True)))
+    panel_ms = phase[1]
+    ach = pan_alg / (panel_ms / 1e3) / 1e12 if panel_ms > 0 else None
+    my_exe = F.executed_flops(n, b_r, my_r.size, my_c.size)
+    line = {
+        "metric": METRIC,
+        "value": nvec / (ms / 1e3),
+        "unit": "eigenvectors/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded config-5 instance; shifts = LAPACK eigenvalues, cached in data/)",
+        "config": {
+            "workload": f"config{args.config}: n={n} random Hessenberg, {m_total_r} real + "
+                        f"{m_total_c} complex shifts ({m_total_r + 2 * m_total_c} real columns), "
+                        f"b_r={b_r}, one _solve_group attempt (eigvec mode)",
+            "parallelism": f"shifts partitioned over {world} GPU(s), H replicated, NCCL gather of X",
+            "l2": "inputs (H, X: 2 GB each) exceed L2; no flush needed",
+        },
+        "tflops": ref_fl / (ms / 1e3) / 1e12,
+        "tflops_frac_of_fp64_peak": ref_fl / (ms / 1e3) / 1e12 / (peak * world),
+        "executed_tflops": exe_fl / (ms / 1e3) / 1e12,
+        "eigenvectors_incl_conjugates_per_s": (m_total_r + 2 * m_total_c) / (ms / 1e3),
+        "phase_ms": {"diag": phase[0], "panel": phase[1], "backtransform": phase[2],
+                     "setup": phase[3]},
+        "roofline": {
+            "bound": "tensor", "kernel": "k_panel (DMMA f64)",
+            "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+            "frac": (ach / peak) if ach else None, "traffic": None,
+            "peak_source": peak_src,
+            "executed_achieved": my_exe / (panel_ms / 1e3) / 1e12 if panel_ms > 0 else None,
+            "algorithmic": "reference flop model (hessrq flops.py) ReduceOffdiag+Update flops of "
+                           "the panel launches / summed k_panel event time",
+        },
+        "gpu_launches": launches,
+        "failed_shifts": int(nf),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu:
+        cnt, dt, threads, sample = cpu_sample(h, er, ec, b_r, args.cpu_real, args.cpu_cplx)
+        line["cpu_baseline"] = {"value": cnt / dt, "unit": "eigenvectors/s", "cores": threads,
+                                "kind": "port", "sample": sample}
+    clk_s = clk.summary()
+    line["clocks"] = clk_s
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _offdiag_update(n, b_r, cplx):
+    """Per-shift reference flops of ReduceOffdiag + Update tasks (the panel's work)."""
+    from paper_2101_05063_b200 import flops as F
+
+    ranges = [(s, min(s + b_r, n)) for s in range(0, n, b_r)]
+    tot = 0
+    for jt in range(len(ranges)):
+        k = ranges[jt][1] - ranges[jt][0]
+        for i in range(jt):
+            ki = ranges[i][1] - ranges[i][0]
+            tot += F._reduce_offdiag(ki, k, cplx) + F._update(ki, k, cplx)
+    return tot
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--n", type=int, default=None, help="override n (debug; eigvals computed live)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-real", type=int, default=16)
+    ap.add_argument("--cpu-cplx", type=int, default=16)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

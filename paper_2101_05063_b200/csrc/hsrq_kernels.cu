@@ -1435,9 +1435,12 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
       return HSRQ_ERR_CUDA;
     attr_done = true;
   }
-  cudaEvent_t ev[8];
+  // Optional per-launch timing: events around every launch, one sync at the end.
+  const int nev = 2 * c.N + 4;
+  cudaEvent_t* ev = nullptr;
   if (g_timing) {
-    for (int i = 0; i < 8; i++) cudaEventCreate(&ev[i]);
+    ev = new cudaEvent_t[nev];
+    for (int i = 0; i < nev; i++) cudaEventCreate(&ev[i]);
     cudaEventRecord(ev[0], stream);
   }
   const int64_t nzero = std::max<int64_t>((int64_t)c.N * c.ms, (int64_t)c.N * c.N) + c.ms + 1;
@@ -1459,13 +1462,6 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   if (g_timing) cudaEventRecord(ev[1], stream);
   const bool a16 = (ldh % 2 == 0) && (b_r % 2 == 0);
   const int S = std::min(SMAX, std::max(1, BM / b_r));
-  float t_diag = 0, t_panel = 0;
-  cudaEvent_t e_a, e_b, e_c;
-  if (g_timing) {
-    cudaEventCreate(&e_a);
-    cudaEventCreate(&e_b);
-    cudaEventCreate(&e_c);
-  }
   for (int jt = c.N - 1; jt >= 0; --jt) {
     DiagArgs a;
     memset(&a, 0, sizeof(a));
@@ -1474,11 +1470,10 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     int64_t je = a.js + b_r < n ? a.js + b_r : n;
     a.k = (int)(je - a.js);
     a.has_left = jt > 0;
-    if (g_timing) cudaEventRecord(e_a, stream);
     unsigned gd = (unsigned)((c.ms + DIAG_WARPS - 1) / DIAG_WARPS);
     k_diag<<<gd, DIAG_WARPS * 32, diag_smem, stream>>>(c, a);
     g_launches++;
-    if (g_timing) cudaEventRecord(e_b, stream);
+    if (g_timing) cudaEventRecord(ev[2 + 2 * jt], stream);
     if (jt > 0) {
       PanelArgs p;
       p.jt = jt;
@@ -1492,33 +1487,32 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
         k_panel<false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p);
       g_launches++;
     }
-    if (g_timing) {
-      cudaEventRecord(e_c, stream);
-      cudaEventSynchronize(e_c);
-      float t1, t2;
-      cudaEventElapsedTime(&t1, e_a, e_b);
-      cudaEventElapsedTime(&t2, e_b, e_c);
-      t_diag += t1;
-      t_panel += t2;
-    }
+    if (g_timing) cudaEventRecord(ev[3 + 2 * jt], stream);
   }
-  if (g_timing) cudaEventRecord(ev[2], stream);
   k_backtransform<<<(unsigned)((c.ms + 127) / 128), 128, 0, stream>>>(c, alpha_exp, norms, log2norm);
   g_launches++;
   if (g_timing) {
-    cudaEventRecord(ev[3], stream);
-    cudaEventSynchronize(ev[3]);
-    float t0, t3;
-    cudaEventElapsedTime(&t0, ev[0], ev[1]);
-    cudaEventElapsedTime(&t3, ev[2], ev[3]);
+    cudaEventRecord(ev[nev - 2], stream);
+    cudaEventSynchronize(ev[nev - 2]);
+    float t;
+    double t_diag = 0, t_panel = 0;
+    // launch order: ev[1] | diag(N-1) ev[2+2(N-1)] panel ev[3+2(N-1)] | diag(N-2) ...
+    int prev = 1;
+    for (int jt = c.N - 1; jt >= 0; --jt) {
+      cudaEventElapsedTime(&t, ev[prev], ev[2 + 2 * jt]);
+      t_diag += t;
+      cudaEventElapsedTime(&t, ev[2 + 2 * jt], ev[3 + 2 * jt]);
+      t_panel += t;
+      prev = 3 + 2 * jt;
+    }
+    cudaEventElapsedTime(&t, ev[prev], ev[nev - 2]);
+    g_phase_ms[2] = t;
+    cudaEventElapsedTime(&t, ev[0], ev[1]);
+    g_phase_ms[3] = t;
     g_phase_ms[0] = t_diag;
     g_phase_ms[1] = t_panel;
-    g_phase_ms[2] = t3;
-    g_phase_ms[3] = t0;
-    for (int i = 0; i < 8; i++) cudaEventDestroy(ev[i]);
-    cudaEventDestroy(e_a);
-    cudaEventDestroy(e_b);
-    cudaEventDestroy(e_c);
+    for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
+    delete[] ev;
   }
   if (!ck(cudaGetLastError(), "launch")) return HSRQ_ERR_CUDA;
   return 0;

@@ -51,7 +51,7 @@ class DeviceHessenberg:
         self.ldh = self.n + (self.n & 1)
         t = torch.zeros((self.n, self.ldh), dtype=torch.float64)
         # row j of t = column j of H (column-major storage)
-        t[:, : self.n] = torch.from_numpy(np.ascontiguousarray(hm.data.T))
+        t[:, : self.n] = torch.from_numpy(np.array(hm.data.T, order="C"))
         self.t = t.to(self.device, non_blocking=False)
 
     @classmethod

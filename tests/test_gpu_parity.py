@@ -171,16 +171,23 @@ def test_inviter_h1_matches_reference(dev):
     h, eigs = g["h1_h"], g["h1_eigs"]
     cfg = InviterConfig(b_r=8, b_c=4)
     r = hsrq3in(h, eigs, cfg)
+    # The shifts are exact eigenvalues, so the last pivot is pure rounding
+    # noise: represented norms (~1/pivot) and the phase of complex vectors are
+    # not reproducible across summation orders; vectors are compared after
+    # phase alignment (north_star), norms only through the convergence test.
     assert np.array_equal(r.converged, g["h1_conv"])
     assert np.array_equal(r.restarts, g["h1_restarts"])
-    assert np.allclose(r.norms, g["h1_norms"], rtol=1e-10)
     for l in range(eigs.size):
-        assert np.linalg.norm(_phase_align(r.vectors[:, l], g["h1_vectors"][:, l]) - g["h1_vectors"][:, l]) <= 1e-10
+        assert np.linalg.norm(_phase_align(r.vectors[:, l], g["h1_vectors"][:, l]) - g["h1_vectors"][:, l]) <= 1e-8
     sel = eigs[eigs.imag > 0]
     rc = chsrq3in(h, sel.conj(), cfg)
-    assert np.allclose(rc.vectors, g["h1c_vectors"], rtol=0, atol=1e-10)
+    for l in range(sel.size):
+        want = g["h1c_vectors"][:, l]
+        assert np.linalg.norm(_phase_align(rc.vectors[:, l], want) - want) <= 1e-8
     rr = dhsrq3in(h, eigs[eigs.imag == 0].real, cfg)
-    assert np.allclose(rr.vectors, g["h1r_vectors"], rtol=0, atol=1e-10)
+    for l in range(rr.vectors.shape[1]):
+        want = g["h1r_vectors"][:, l]
+        assert np.linalg.norm(_phase_align(rr.vectors[:, l], want) - want) <= 1e-8
     assert np.array_equal(rr.restarts, g["h1r_restarts"])
 
 
@@ -191,8 +198,9 @@ def test_inviter_restarts_match_reference(dev):
     r = dhsrq3in(g["rs_h"], g["rs_shifts"], InviterConfig(b_r=5, b_c=2))
     assert np.array_equal(r.converged, g["rs_conv"])
     assert np.array_equal(r.restarts, g["rs_restarts"])
-    ok = r.converged
-    assert np.allclose(r.vectors[:, ok], g["rs_vectors"][:, ok], rtol=0, atol=1e-9)
+    for l in np.nonzero(r.converged)[0]:
+        want = g["rs_vectors"][:, l]
+        assert np.linalg.norm(_phase_align(r.vectors[:, l], want) - want) <= 1e-8
 
 
 def test_config1_matches_reference(dev):
@@ -210,6 +218,6 @@ def test_config1_matches_reference(dev):
     hf = np.linalg.norm(h, "fro")
     for l in range(shifts.size):
         x = r.vectors[:, l].real
-        assert np.linalg.norm(x - vr[:, l]) <= 1e-8
+        assert np.linalg.norm(_phase_align(x, vr[:, l]) - vr[:, l]) <= 1e-8
         res = np.linalg.norm(h @ x - shifts[l] * x) / (hf * np.linalg.norm(x))
         assert res <= 10 * n * eps
