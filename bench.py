@@ -318,6 +318,27 @@ def run_gpu(args):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": ems}
 
+    # ---- correctness on this rank's shard: convergence of every column and the
+    # north_star residual bound on a sample (the last step's X is the result) ----
+    norms_all = gs.norms.cpu().numpy()
+    conv = int(np.count_nonzero(norms_all > 0.1 / np.sqrt(n)))
+    rng = np.random.default_rng(5)
+    samp_c = rng.choice(my_c.size, min(6, my_c.size), replace=False) if my_c.size else []
+    samp_r = rng.choice(my_r.size, min(6, my_r.size), replace=False) if my_r.size else []
+    hf = np.linalg.norm(h, "fro")
+    worst = 0.0
+    Xs = gs.X
+    for i in samp_c:
+        x = Xs[2 * i].cpu().numpy() + 1j * Xs[2 * i + 1].cpu().numpy()
+        worst = max(worst, np.linalg.norm(h @ x - my_c[i] * x) / (hf * np.linalg.norm(x)))
+    for i in samp_r:
+        x = Xs[2 * my_c.size + i].cpu().numpy()
+        worst = max(worst, np.linalg.norm(h @ x - my_r[i] * x) / (hf * np.linalg.norm(x)))
+    check = {"converged": conv, "shifts": int(gs.ms),
+             "max_residual_over_n_eps": worst / (n * np.finfo(float).eps),
+             "residual_sample": len(samp_c) + len(samp_r),
+             "bound": "||Hx-lx||/(||H||_F ||x||) <= 10 n eps"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -372,6 +393,7 @@ def run_gpu(args):
         },
         "gpu_launches": launches,
         "failed_shifts": int(nf),
+        "check": check,
     }
     if e2e:
         line["e2e"] = e2e

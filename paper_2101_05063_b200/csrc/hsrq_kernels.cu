@@ -79,6 +79,8 @@ struct Ctx {
   StepScalars* SS;       // ms
   double* HM0;           // N x N : max |H[tile i rows, js-1]|
   double* RS;            // N x N : max row sum |H[tile i rows, js:je-1]|
+  double* XB;            // N x ms: max |X| over each tile's rows (real: exact;
+                         // complex: max(|re|+|im|), an upper bound of max |x|)
   int64_t* fail;         // ms
   unsigned long long* nfail;
   int robust, mode;
@@ -128,6 +130,11 @@ __global__ void k_init(Ctx c, const double* B, int64_t ldb, int b_broadcast) {
   int64_t q = cplx ? col / 2 : c.mc + (col - 2 * c.mc);
   double b = b_broadcast ? (im ? 0.0 : B[r]) : B[col * ldb + r];
   c.X[col * c.ldx + r] = b;
+  if (!im) {
+    double bb = fabs(b);
+    if (cplx && !b_broadcast) bb = bb + fabs(B[(col + 1) * ldb + r]);
+    atomicMax((unsigned long long*)&c.XB[(r / c.b_r) * c.ms + q], dkey(bb));
+  }
   double h = im ? 0.0 : c.H[(c.n - 1) * c.ldh + r];
   if (r == c.n - 1) h -= im ? c.lam_im[q] : c.lam_re[q];
   c.Cr[col * c.ldx + r] = h;
@@ -136,7 +143,10 @@ __global__ void k_init(Ctx c, const double* B, int64_t ldb, int b_broadcast) {
 __global__ void k_zero_state(Ctx c) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t ne = (int64_t)c.N * c.ms;
-  if (t < ne) c.E[t] = 0;
+  if (t < ne) {
+    c.E[t] = 0;
+    c.XB[t] = 0.0;
+  }
   if (t < c.ms) c.fail[t] = 0;
   if (t < (int64_t)c.N * c.N) {
     c.HM0[t] = 0.0;
@@ -737,574 +747,9 @@ __global__ void __launch_bounds__(DIAG_WARPS * 32) k_diag(Ctx c, DiagArgs a) {
     diag_real(c, a, sm, q, col, warp, hleft0);
 }
 
-// ---------------------------------------------------------------------------
-// k_panel: fused reduction + guarded update GEMM on DMMA
-// ---------------------------------------------------------------------------
+#include "hsrq_panel.cuh"
 
-struct PanelArgs {
-  int jt;
-  int64_t js;
-  int k;            // width of tile column jt (K)
-  int S;            // tile rows per CTA
-};
-
-struct PanelSmem {
-  union {
-    struct {
-      double A[STAGES][BK][APAD];
-      double B[STAGES][2 * BN][BPAD];
-    } pipe;
-    double C[2 * BN][APAD];  // accumulators, [acc col][row]
-  } u;
-  unsigned long long red[2][SMAX][BN];
-  double fb[SMAX][BN], rr[SMAX][BN], ri[SMAX][BN], fx[SMAX][BN], xi2[SMAX][BN];
-  double zkr[SMAX][BN], zki[SMAX][BN], xi3[SMAX][BN];
-  int dexp[SMAX][BN];
-};
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  int sz = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-__device__ __forceinline__ void mma_f64(double (&d)[4], double a0, double a1, double b0) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
-      "{%0,%1,%2,%3};\n"
-      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
-      : "d"(a0), "d"(a1), "d"(b0));
-}
-
-// Loads one K chunk of A (rows row0.., H columns js-1+kc*BK..) and B.
-template <bool A16>
-__device__ __forceinline__ void panel_load(const Ctx& c, const PanelArgs& p, PanelSmem& sm,
-                                           int stage, int kc, int64_t row0, int rows_valid,
-                                           int64_t col0) {
-  const int tid = threadIdx.x;
-  // A: BK columns x BM rows
-  if (A16) {
-#pragma unroll
-    for (int it = 0; it < (BK * BM / 2) / PANEL_THREADS; it++) {
-      int e = tid + it * PANEL_THREADS;  // 16-byte chunk index
-      int kk = e / (BM / 2);
-      int m2 = (e % (BM / 2)) * 2;
-      int kglob = kc * BK + kk;
-      bool valid = kglob < p.k && m2 < rows_valid;
-      const double* src = c.H + (p.js - 1 + (valid ? kglob : 0)) * c.ldh + row0 + (valid ? m2 : 0);
-      cp_async16(&sm.u.pipe.A[stage][kk][m2], src, valid);
-    }
-  } else {
-#pragma unroll
-    for (int it = 0; it < (BK * BM) / PANEL_THREADS; it++) {
-      int e = tid + it * PANEL_THREADS;
-      int kk = e / BM;
-      int m = e % BM;
-      int kglob = kc * BK + kk;
-      bool valid = kglob < p.k && m < rows_valid;
-      const double* src = c.H + (p.js - 1 + (valid ? kglob : 0)) * c.ldh + row0 + (valid ? m : 0);
-      cp_async8(&sm.u.pipe.A[stage][kk][m], src, valid);
-    }
-  }
-  // B: 2*BN accumulator columns x BK
-#pragma unroll
-  for (int it = 0; it < (2 * BN * BK / 2) / PANEL_THREADS; it++) {
-    int e = tid + it * PANEL_THREADS;
-    int nn = e / (BK / 2);
-    int k2 = (e % (BK / 2)) * 2;
-    const double* src = c.Bop + (2 * col0 + nn) * KP + kc * BK + k2;
-    cp_async16(&sm.u.pipe.B[stage][nn][k2], src, true);
-  }
-}
-
-// Column bookkeeping for a data column of this CTA.
-struct ColInfo {
-  bool valid, cplx, im;
-  int64_t col, partner, q;
-};
-__device__ __forceinline__ ColInfo col_info(const Ctx& c, int64_t col) {
-  ColInfo ci;
-  ci.col = col;
-  ci.valid = col < c.ncol;
-  ci.cplx = col < 2 * c.mc;
-  ci.im = ci.cplx && (col & 1);
-  ci.partner = ci.cplx ? (col ^ 1) : col;
-  ci.q = ci.cplx ? col / 2 : c.mc + (col - 2 * c.mc);
-  return ci;
-}
-
-template <bool A16>
-__global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  PanelSmem& sm = *reinterpret_cast<PanelSmem*>(smem_raw);
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int S = p.S;
-  const int tile0 = blockIdx.y * S;                  // first tile row of this CTA
-  const int ntiles = min(S, p.jt - tile0);           // tile rows here (all above jt)
-  const int64_t row0 = (int64_t)tile0 * c.b_r;
-  const int rows_valid = ntiles * c.b_r;
-  const int64_t col0 = (int64_t)blockIdx.x * BN;
-  const int nk = (p.k + BK - 1) / BK;
-  const int jt = p.jt;
-  const double omega = c.omega;
-  const bool robust = c.robust;
-
-  // start the pipeline
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; s++) {
-    if (s < nk) panel_load<A16>(c, p, sm, s, s, row0, rows_valid, col0);
-    cp_commit();
-  }
-
-  // ---------------- prologue: update steps 1 and 2 guards ----------------
-  // thread -> (data column cl = tid / 8, row part rp = tid % 8: rows rp + 8*j)
-  const int cl = tid >> 3, rp = tid & 7;
-  const ColInfo ci = col_info(c, col0 + cl);
-  for (int e = tid; e < 2 * SMAX * BN; e += PANEL_THREADS) (&sm.red[0][0][0])[e] = 0ULL;
-  __syncthreads();
-  if (ci.valid) {
-    // step-1 bmax (update_rupdate :214-217 / cupdate :609-613)
-    double lm = 0.0;
-    int seg = -1;
-    for (int r = rp; r < rows_valid; r += 8) {
-      int sg = r / c.b_r;
-      if (sg != seg) {
-        if (seg >= 0) atomicMax(&sm.red[0][seg][cl], dkey(lm));
-        seg = sg;
-        lm = 0.0;
-      }
-      double xv = c.X[ci.col * c.ldx + row0 + r];
-      double q = ci.cplx ? ghypot(c.X[(ci.col & ~1LL) * c.ldx + row0 + r],
-                                  c.X[(ci.col | 1LL) * c.ldx + row0 + r])
-                         : fabs(xv);
-      if (q > lm) lm = q;
-    }
-    if (seg >= 0) atomicMax(&sm.red[0][seg][cl], dkey(lm));
-  }
-  __syncthreads();
-  // per (segment, column) step-1 scalars
-  for (int e = tid; e < S * BN; e += PANEL_THREADS) {
-    int sg = e / BN, cc = e % BN;
-    ColInfo cj = col_info(c, col0 + cc);
-    if (!cj.valid || sg >= ntiles) continue;
-    int it = tile0 + sg;
-    const StepScalars st = c.SS[cj.q];
-    const int ae = c.E[(int64_t)jt * c.ms + cj.q];
-    const int be = c.E[(int64_t)it * c.ms + cj.q];
-    const bool shifted = it == jt - 1;
-    double fbv = 1.0, fxv = 1.0, rre = st.rho_re, rim = st.rho_im;
-    int d = 0;
-    if (robust) {
-      const int g = ae < be ? ae : be;
-      const double bmax = dval(sm.red[0][sg][cc]);
-      const double alam = shifted ? (cj.cplx ? ghypot(c.lam_re[cj.q], c.lam_im[cj.q])
-                                             : fabs(c.lam_re[cj.q]))
-                                  : 0.0;
-      const double hm0 = c.HM0[(int64_t)jt * c.N + it];
-      const double arho = cj.cplx ? ghypot(rre, rim) : fabs(rre);
-      const int xe = protect_update_e(p2(g - be) * bmax, hm0 + alam, arho, omega);
-      d = xe + g;
-      fbv = p2(d - be);
-      fxv = p2(d - ae);
-      if (fxv != 1.0) {
-        rre = fxv * rre;
-        rim = fxv * rim;
-      }
-    }
-    sm.fb[sg][cc] = fbv;
-    sm.fx[sg][cc] = fxv;
-    sm.rr[sg][cc] = rre;
-    sm.ri[sg][cc] = rim;
-    sm.dexp[sg][cc] = d;
-  }
-  __syncthreads();
-  // step-1 application and the step-2 bmax (:224-231, :264-267)
-  if (ci.valid && robust) {
-    double lm = 0.0;
-    int seg = -1;
-    for (int r = rp; r < rows_valid; r += 8) {
-      int sg = r / c.b_r;
-      if (sg != seg) {
-        if (seg >= 0) atomicMax(&sm.red[1][seg][cl], dkey(lm));
-        seg = sg;
-        lm = 0.0;
-      }
-      const int64_t grow = row0 + r;
-      const double h0 = c.H[(p.js - 1) * c.ldh + grow];
-      const bool last = ((r + 1) % c.b_r == 0) && (tile0 + sg == jt - 1);
-      const double fbv = sm.fb[sg][cl];
-      double q;
-      if (ci.cplx) {
-        const int64_t cr_ = ci.col & ~1LL;
-        double xr = c.X[cr_ * c.ldx + grow], xi = c.X[(cr_ + 1) * c.ldx + grow];
-        if (fbv != 1.0) {
-          xr *= fbv;
-          xi *= fbv;
-        }
-        const double rre = sm.rr[sg][cl], rim = sm.ri[sg][cl];
-        xr += rre * h0;
-        xi += rim * h0;
-        if (last) {
-          const double lr = c.lam_re[ci.q], li = c.lam_im[ci.q];
-          xr -= lr * rre - li * rim;
-          xi -= lr * rim + li * rre;
-        }
-        q = ghypot(xr, xi);
-      } else {
-        double xv = c.X[ci.col * c.ldx + grow];
-        if (fbv != 1.0) xv *= fbv;
-        const double rho = sm.rr[sg][cl];
-        xv += rho * h0;
-        if (last) xv -= c.lam_re[ci.q] * rho;
-        q = fabs(xv);
-      }
-      if (q > lm) lm = q;
-    }
-    if (seg >= 0) atomicMax(&sm.red[1][seg][cl], dkey(lm));
-  }
-  __syncthreads();
-  for (int e = tid; e < S * BN; e += PANEL_THREADS) {
-    int sg = e / BN, cc = e % BN;
-    ColInfo cj = col_info(c, col0 + cc);
-    if (!cj.valid || sg >= ntiles) continue;
-    int it = tile0 + sg;
-    const StepScalars st = c.SS[cj.q];
-    const double fxv = sm.fx[sg][cc];
-    double zr = st.zk_re, zi = st.zk_im;
-    if (fxv != 1.0) {
-      zr *= fxv;
-      zi *= fxv;
-    }
-    double x2 = 1.0;
-    if (robust && p.k > 1) {
-      const double zmax = fxv != 1.0 ? fxv * st.zmax : st.zmax;
-      const int xe = protect_update_e(dval(sm.red[1][sg][cc]), c.RS[(int64_t)jt * c.N + it], zmax,
-                                      omega);
-      if (xe < 0) {
-        x2 = p2(xe);
-        sm.dexp[sg][cc] += xe;
-        zr *= x2;
-        zi *= x2;
-      }
-    }
-    sm.xi2[sg][cc] = x2;
-    sm.zkr[sg][cc] = zr;
-    sm.zki[sg][cc] = zi;
-  }
-  // (the __syncthreads of the main loop orders these before the epilogue)
-
-  // ---------------- main loop: acc = A * [W | Zs] on DMMA ----------------
-  const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps, warp tile 32 rows x 32 acc cols
-  const int g = lane >> 2, t4 = lane & 3;
-  double acc[2][4][4];
-#pragma unroll
-  for (int i = 0; i < 2; i++)
-#pragma unroll
-    for (int j = 0; j < 4; j++)
-#pragma unroll
-      for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
-
-  for (int kc = 0; kc < nk; kc++) {
-    cp_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      int nxt = kc + STAGES - 1;
-      if (nxt < nk) panel_load<A16>(c, p, sm, nxt % STAGES, nxt, row0, rows_valid, col0);
-      cp_commit();
-    }
-    const int st = kc % STAGES;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[2][2], bf[4];
-#pragma unroll
-      for (int mi = 0; mi < 2; mi++) {
-        int r = wm * 32 + mi * 16 + g;
-        af[mi][0] = sm.u.pipe.A[st][kk + t4][r];
-        af[mi][1] = sm.u.pipe.A[st][kk + t4][r + 8];
-      }
-#pragma unroll
-      for (int ni = 0; ni < 4; ni++) bf[ni] = sm.u.pipe.B[st][wn * 32 + ni * 8 + g][kk + t4];
-#pragma unroll
-      for (int mi = 0; mi < 2; mi++)
-#pragma unroll
-        for (int ni = 0; ni < 4; ni++) mma_f64(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
-    }
-  }
-  cp_wait<0>();
-  __syncthreads();
-  // stage accumulators: C[acc col][row]
-#pragma unroll
-  for (int mi = 0; mi < 2; mi++)
-#pragma unroll
-    for (int ni = 0; ni < 4; ni++) {
-      int r = wm * 32 + mi * 16 + g;
-      int cc = wn * 32 + ni * 8 + 2 * t4;
-      sm.u.C[cc][r] = acc[mi][ni][0];
-      sm.u.C[cc + 1][r] = acc[mi][ni][1];
-      sm.u.C[cc][r + 8] = acc[mi][ni][2];
-      sm.u.C[cc + 1][r + 8] = acc[mi][ni][3];
-    }
-  for (int e = tid; e < 2 * SMAX * BN; e += PANEL_THREADS) (&sm.red[0][0][0])[e] = 0ULL;
-  __syncthreads();
-
-  // ---------------- epilogue ----------------
-  // X'' = xi2 * X' - (fx xi2) (A Z);  guards of step 3 need max|X''| and max|Cr_old|.
-  constexpr int RPT = BM / 8;  // rows per thread
-  double xo[RPT];  // X'' (own part) kept across the step-3 reduction
-  if (ci.valid) {
-    double lmb = 0.0, lmr = 0.0;
-    int seg = -1;
-#pragma unroll
-    for (int j = 0; j < RPT; j++) {
-      int r = rp + 8 * j;
-      xo[j] = 0.0;
-      if (r >= rows_valid) continue;
-      int sg = r / c.b_r;
-      if (sg != seg) {
-        if (seg >= 0) {
-          atomicMax(&sm.red[0][seg][cl], dkey(lmb));
-          atomicMax(&sm.red[1][seg][cl], dkey(lmr));
-        }
-        seg = sg;
-        lmb = lmr = 0.0;
-      }
-      const int64_t grow = row0 + r;
-      const double h0 = c.H[(p.js - 1) * c.ldh + grow];
-      const bool last = ((r + 1) % c.b_r == 0) && (tile0 + sg == jt - 1);
-      const double fbv = sm.fb[sg][cl], x2 = sm.xi2[sg][cl];
-      const double pz = sm.fx[sg][cl] * x2;
-      if (ci.cplx) {
-        const int64_t cre_ = ci.col & ~1LL;
-        const int cl_re = cl & ~1;
-        double xr = c.X[cre_ * c.ldx + grow], xi = c.X[(cre_ + 1) * c.ldx + grow];
-        if (fbv != 1.0) {
-          xr *= fbv;
-          xi *= fbv;
-        }
-        const double rre = sm.rr[sg][cl], rim = sm.ri[sg][cl];
-        xr += rre * h0;
-        xi += rim * h0;
-        if (last) {
-          const double lr = c.lam_re[ci.q], li = c.lam_im[ci.q];
-          xr -= lr * rre - li * rim;
-          xi -= lr * rim + li * rre;
-        }
-        if (x2 < 1.0) {
-          xr *= x2;
-          xi *= x2;
-        }
-        xr -= pz * sm.u.C[2 * cl_re + 1][r];
-        xi -= pz * sm.u.C[2 * (cl_re + 1) + 1][r];
-        const double cr_r = c.Cr[cre_ * c.ldx + grow], cr_i = c.Cr[(cre_ + 1) * c.ldx + grow];
-        xo[j] = ci.im ? xi : xr;
-        double qb = ghypot(xr, xi), qr = ghypot(cr_r, cr_i);
-        if (qb > lmb) lmb = qb;
-        if (qr > lmr) lmr = qr;
-      } else {
-        double xv = c.X[ci.col * c.ldx + grow];
-        if (fbv != 1.0) xv *= fbv;
-        const double rho = sm.rr[sg][cl];
-        xv += rho * h0;
-        if (last) xv -= c.lam_re[ci.q] * rho;
-        if (x2 < 1.0) xv *= x2;
-        xv -= pz * sm.u.C[2 * cl + 1][r];
-        const double crv = c.Cr[ci.col * c.ldx + grow];
-        xo[j] = xv;
-        if (fabs(xv) > lmb) lmb = fabs(xv);
-        if (fabs(crv) > lmr) lmr = fabs(crv);
-      }
-    }
-    if (seg >= 0) {
-      atomicMax(&sm.red[0][seg][cl], dkey(lmb));
-      atomicMax(&sm.red[1][seg][cl], dkey(lmr));
-    }
-  }
-  __syncthreads();
-  // step 3 guard (:287-301) and the new beta
-  for (int e = tid; e < S * BN; e += PANEL_THREADS) {
-    int sg = e / BN, cc = e % BN;
-    ColInfo cj = col_info(c, col0 + cc);
-    if (!cj.valid || sg >= ntiles) continue;
-    double zr = sm.zkr[sg][cc], zi = sm.zki[sg][cc];
-    double x3 = 1.0;
-    if (robust) {
-      const double az = cj.cplx ? ghypot(zr, zi) : fabs(zr);
-      const int xe = protect_update_e(dval(sm.red[0][sg][cc]), dval(sm.red[1][sg][cc]), az, omega);
-      if (xe < 0) {
-        x3 = p2(xe);
-        sm.dexp[sg][cc] += xe;
-        zr *= x3;
-        zi *= x3;
-      }
-      if (!cj.im) c.E[(int64_t)(tile0 + sg) * c.ms + cj.q] = sm.dexp[sg][cc];
-    }
-    sm.xi3[sg][cc] = x3;
-    sm.zkr[sg][cc] = zr;
-    sm.zki[sg][cc] = zi;
-  }
-  __syncthreads();
-  if (ci.valid) {
-    const StepScalars st = c.SS[ci.q];
-#pragma unroll
-    for (int j = 0; j < RPT; j++) {
-      int r = rp + 8 * j;
-      if (r >= rows_valid) continue;
-      int sg = r / c.b_r;
-      const int64_t grow = row0 + r;
-      const double x3 = sm.xi3[sg][cl];
-      const double zr = sm.zkr[sg][cl], zi = sm.zki[sg][cl];
-      double xv = xo[j];
-      if (x3 < 1.0) xv *= x3;
-      double crn;
-      const bool lastrow = (grow == p.js - 1);
-      if (ci.cplx) {
-        const int64_t cre_ = ci.col & ~1LL;
-        const double crr = c.Cr[cre_ * c.ldx + grow], cri = c.Cr[(cre_ + 1) * c.ldx + grow];
-        if (ci.im)
-          xv -= crr * zi + cri * zr;
-        else
-          xv -= crr * zr - cri * zi;
-        crn = sm.u.C[2 * cl][r] + st.P * (ci.im ? cri : crr);
-        if (lastrow) {
-          const double lr = c.lam_re[ci.q], li = c.lam_im[ci.q];
-          crn -= ci.im ? (st.c0_re * li + st.c0_im * lr) : (st.c0_re * lr - st.c0_im * li);
-        }
-      } else {
-        const double crv = c.Cr[ci.col * c.ldx + grow];
-        xv -= crv * zr;
-        crn = sm.u.C[2 * cl][r] + st.P * crv;
-        if (lastrow) crn -= st.c0_re * c.lam_re[ci.q];
-      }
-      c.X[ci.col * c.ldx + grow] = xv;
-      c.Cr[ci.col * c.ldx + grow] = crn;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// k_backtransform: rbacktransform / crbacktransform, one thread per shift
-// ---------------------------------------------------------------------------
-__global__ void k_backtransform(Ctx c, int32_t* alpha_exp, double* norms, double* log2norm) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= c.ms) return;
-  bool cplx;
-  int64_t col;
-  col_of_shift(c, q, cplx, col);
-  const int64_t n = c.n;
-  double* xr = c.X + col * c.ldx;
-  double* xi = cplx ? c.X + (col + 1) * c.ldx : nullptr;
-  const double* cr = c.c_re + q * c.ldc;
-  const double* ci = cplx ? c.c_im + q * c.ldc : nullptr;
-  const double* ss = c.s + q * c.ldc;
-  if (c.fail[q] != 0) {
-    norms[q] = __longlong_as_double(0x7ff8000000000000LL);
-    log2norm[q] = norms[q];
-    alpha_exp[q] = 0;
-    return;
-  }
-  if (!c.robust) {  // backtransform / cbacktransform (:314-323, :739-756)
-    norms[q] = __longlong_as_double(0x7ff8000000000000LL);
-    log2norm[q] = norms[q];
-    alpha_exp[q] = 0;
-  } else {
-    int amin = c.E[q];
-    for (int t = 1; t < c.N; t++) {
-      int e = c.E[(int64_t)t * c.ms + q];
-      if (e < amin) amin = e;
-    }
-    for (int t = 0; t < c.N; t++) {
-      double f = p2(amin - c.E[(int64_t)t * c.ms + q]);
-      if (f != 1.0) {
-        int64_t s0 = (int64_t)t * c.b_r, s1 = s0 + c.b_r < n ? s0 + c.b_r : n;
-        for (int64_t i = s0; i < s1; i++) {
-          xr[i] *= f;
-          if (cplx) xi[i] *= f;
-        }
-      }
-    }
-    double xmax = 0.0;
-    for (int64_t i = 0; i < n; i++) {
-      double qv = cplx ? ghypot(xr[i], xi[i]) : fabs(xr[i]);
-      if (qv > xmax) xmax = qv;
-    }
-    if (xmax == 0.0) {
-      norms[q] = 0.0;
-      log2norm[q] = -__longlong_as_double(0x7ff0000000000000LL);
-      alpha_exp[q] = amin;
-      return;
-    }
-    double tsum = 0.0;
-    for (int64_t i = 0; i < n; i++) {
-      if (cplx) {
-        double qr = xr[i] / xmax, qi = xi[i] / xmax;
-        tsum += qr * qr + qi * qi;
-      } else {
-        double qv = xr[i] / xmax;
-        tsum += qv * qv;
-      }
-    }
-    double rt = sqrt(tsum);
-    norms[q] = ldexp(xmax, -amin) * rt;
-    log2norm[q] = log2(xmax) + log2(rt) - (double)amin;
-    alpha_exp[q] = amin;
-    if (c.mode == 1) {
-      for (int64_t i = 0; i < n; i++) {
-        xr[i] /= xmax;
-        if (cplx) xi[i] /= xmax;
-      }
-      for (int64_t i = 0; i < n; i++) {
-        xr[i] /= rt;
-        if (cplx) xi[i] /= rt;
-      }
-    } else {
-      double qq = c.omega / xmax;
-      if (rt > qq) {
-        int e = pow2floor_e(qq / rt);
-        double f = p2(e);
-        for (int64_t i = 0; i < n; i++) {
-          xr[i] *= f;
-          if (cplx) xi[i] *= f;
-        }
-        alpha_exp[q] = amin + e;
-      }
-    }
-  }
-  // rotation sweep
-  if (cplx) {
-    double t1r = xr[0], t1i = xi[0];
-    for (int64_t i = 1; i < n; i++) {
-      double c_r = cr[i], c_i = ci[i], sv = ss[i];
-      double t2r = xr[i], t2i = xi[i];
-      xr[i - 1] = (c_r * t1r - c_i * t1i) - sv * t2r;
-      xi[i - 1] = (c_r * t1i + c_i * t1r) - sv * t2i;
-      double nr = sv * t1r + (c_r * t2r + c_i * t2i);
-      double ni = sv * t1i + (c_r * t2i - c_i * t2r);
-      t1r = nr;
-      t1i = ni;
-    }
-    xr[n - 1] = t1r;
-    xi[n - 1] = t1i;
-  } else {
-    double t1 = xr[0];
-    for (int64_t i = 1; i < n; i++) {
-      double t2 = xr[i];
-      xr[i - 1] = cr[i] * t1 - ss[i] * t2;
-      t1 = cr[i] * t2 + ss[i] * t1;
-    }
-    xr[n - 1] = t1;
-  }
-}
+#include "hsrq_backtransform.cuh"
 
 // elementwise helpers for parity tests
 __global__ void k_protect_batch(const double* b, const double* h, const double* x, double omega,
@@ -1340,7 +785,7 @@ bool ck(cudaError_t e, const char* what) {
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t cr, bop, ss, hm0, rs, nfail, total;
+  size_t cr, bop, ss, hm0, rs, xb, rsc, nfail, total;
 };
 
 WsLayout ws_layout(int64_t n, int b_r, int64_t mc, int64_t mr) {
@@ -1362,6 +807,10 @@ WsLayout ws_layout(int64_t n, int b_r, int64_t mc, int64_t mr) {
   off = align_up(off + sizeof(double) * (size_t)N * N, 256);
   L.rs = off;
   off = align_up(off + sizeof(double) * (size_t)N * N, 256);
+  L.xb = off;
+  off = align_up(off + sizeof(double) * (size_t)N * ms, 256);
+  L.rsc = off;
+  off = align_up(off + 64 * (size_t)N * ms, 256);
   L.total = off;
   return L;
 }
@@ -1406,6 +855,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   c.SS = (StepScalars*)(w + L.ss);
   c.HM0 = (double*)(w + L.hm0);
   c.RS = (double*)(w + L.rs);
+  c.XB = (double*)(w + L.xb);
   c.fail = fail;
   c.nfail = (unsigned long long*)(w + L.nfail);
   c.robust = robust;
@@ -1423,15 +873,15 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   const size_t panel_smem = sizeof(PanelSmem);
   if (!attr_done) {
     if (!ck(cudaFuncSetAttribute(k_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem),
-            "attr diag"))
-      return HSRQ_ERR_CUDA;
-    if (!ck(cudaFuncSetAttribute(k_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)panel_smem),
-            "attr panel"))
-      return HSRQ_ERR_CUDA;
-    if (!ck(cudaFuncSetAttribute(k_panel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)panel_smem),
-            "attr panel8"))
+            "attr diag") ||
+        !ck(cudaFuncSetAttribute(k_panel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)panel_smem), "attr panel") ||
+        !ck(cudaFuncSetAttribute(k_panel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)panel_smem), "attr panel") ||
+        !ck(cudaFuncSetAttribute(k_panel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)panel_smem), "attr panel") ||
+        !ck(cudaFuncSetAttribute(k_panel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)panel_smem), "attr panel"))
       return HSRQ_ERR_CUDA;
     attr_done = true;
   }
@@ -1480,16 +930,26 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
       p.js = a.js;
       p.k = a.k;
       p.S = S;
+      RowScalars* rsc = (RowScalars*)(w + L.rsc);
+      const int64_t nsc = (int64_t)jt * c.ms;
+      k_scalars<<<(unsigned)((nsc + 127) / 128), 128, 0, stream>>>(c, p, rsc);
+      g_launches++;
       dim3 gp((unsigned)(c.ncol_pad / BN), (unsigned)((jt + S - 1) / S));
-      if (a16)
-        k_panel<true><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p);
+      const bool seg16 = (b_r % 16) == 0;
+      if (a16 && seg16)
+        k_panel<true, true><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
+      else if (a16)
+        k_panel<true, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
+      else if (seg16)
+        k_panel<false, true><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
       else
-        k_panel<false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p);
+        k_panel<false, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
       g_launches++;
     }
     if (g_timing) cudaEventRecord(ev[3 + 2 * jt], stream);
   }
-  k_backtransform<<<(unsigned)((c.ms + 127) / 128), 128, 0, stream>>>(c, alpha_exp, norms, log2norm);
+  k_backtransform<<<(unsigned)((c.ms + BT_WARPS - 1) / BT_WARPS), BT_WARPS * 32, 0, stream>>>(
+      c, alpha_exp, norms, log2norm);
   g_launches++;
   if (g_timing) {
     cudaEventRecord(ev[nev - 2], stream);

@@ -1,0 +1,589 @@
+// hsrq_panel.cuh -- k_scalars + k_panel: the shared off-diagonal work of one
+// tile column as ONE fp64 tensor-core GEMM over every shift (included by
+// hsrq_kernels.cu).
+//
+// For tile column jt (rows js..je, k = je - js) and every tile row i < jt:
+//   reduction  Cr(:, jt-1) = A W + diag(P) Cr(:, jt) - c0 lambda e_{js-1}
+//              (reduce_offdiag, numba_backend.py:109-125, as a linear map)
+//   update     the three ProtectUpdate-guarded steps of update_rupdate /
+//              cupdate_crupdate (numba_backend.py:198-311, :579-736) with
+//              step 2's GEMM  b -= H(:, 1:k) Z(0:k-1)  (:279-285)
+// with A = H[0:js, js-1:je-1] shared by both products: the B operand holds
+// [W_c | Zs_c] for every real column c, so acc = A [W | Zs] is one DMMA GEMM
+// (mma.sync m16n8k4 f64 -> DMMA.8x8x4 on sm_100a).
+//
+// Guards are evaluated bound-first: protect_update is monotone in its
+// arguments, so an upper bound that already yields xi == 1 proves the exact
+// value is 1; exact maxima (hypot for complex columns) are formed only when
+// a bound fails, i.e. near overflow.  k_scalars resolves steps 1 and 2 per
+// (tile row, shift) before the GEMM (their inputs are known then); a panel
+// CTA owns whole tile rows, so step 3 -- which needs the GEMM result -- is
+// CTA-local in the epilogue.
+
+struct PanelArgs {
+  int jt;
+  int64_t js;
+  int k;  // width of tile column jt (GEMM K)
+  int S;  // tile rows per CTA
+};
+
+// Per (tile row, shift) scalars of update steps 1-2, written by k_scalars.
+struct RowScalars {
+  double fb;        // beta -> delta rescale of b          (:221-226)
+  double fx;        // alpha -> delta rescale of x / Z       (:222, :240-245)
+  double rr, ri;    // rho = fx * s0 * xbelow[0]            (:227)
+  double x2;        // step-2 xi                            (:272-278)
+  double zkr, zki;  // Z[k-1] * fx * x2                     (:302)
+  int dexp;         // log2(delta) after step 2
+  int pad;
+};
+
+constexpr double BOUND_SLACK = 1.0 + 0x1p-46;  // covers the roundings inside a bound
+
+// X' = fb X + rho h0 (- lambda rho on the last row of the shifted tile):
+// update_rupdate :224-231 / cupdate_crupdate :621-633, one component.
+__device__ __forceinline__ double step1_apply(double x, double fb, double rr, double ri, double h0,
+                                              bool last, bool cplx, bool im, double lr, double li) {
+  if (fb != 1.0) x *= fb;
+  if (!cplx) {
+    x += rr * h0;
+    if (last) x -= lr * rr;
+    return x;
+  }
+  if (im) {
+    x += ri * h0;
+    if (last) x -= lr * ri + li * rr;
+  } else {
+    x += rr * h0;
+    if (last) x -= lr * rr - li * ri;
+  }
+  return x;
+}
+
+// One thread per (tile row it < jt, shift q).
+__global__ void k_scalars(Ctx c, PanelArgs p, RowScalars* RSc) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int jt = p.jt;
+  if (t >= (int64_t)jt * c.ms) return;
+  const int it = (int)(t / c.ms);
+  const int64_t q = t % c.ms;
+  const bool cplx = q < c.mc;
+  const int64_t col = cplx ? 2 * q : 2 * c.mc + (q - c.mc);
+  const StepScalars st = c.SS[q];
+  RowScalars o;
+  o.pad = 0;
+  if (c.fail[q] != 0 || !c.robust) {
+    o.fb = o.fx = o.x2 = 1.0;
+    o.rr = st.rho_re;
+    o.ri = st.rho_im;
+    o.zkr = st.zk_re;
+    o.zki = st.zk_im;
+    o.dexp = 0;
+    RSc[t] = o;
+    return;
+  }
+  const double omega = c.omega;
+  const bool shifted = it == jt - 1;
+  const double lr = c.lam_re[q], li = cplx ? c.lam_im[q] : 0.0;
+  const int64_t r0 = (int64_t)it * c.b_r;
+  const int ae = c.E[(int64_t)jt * c.ms + q];
+  const int be = c.E[(int64_t)it * c.ms + q];
+  const int g = ae < be ? ae : be;
+  const double alam = shifted ? (cplx ? ghypot(lr, li) : fabs(lr)) : 0.0;
+  const double hm0 = c.HM0[(int64_t)jt * c.N + it];
+  const double arho = cplx ? ghypot(st.rho_re, st.rho_im) : fabs(st.rho_re);
+  // ---- step 1 (:211-231) ----
+  double bmax = c.XB[(int64_t)it * c.ms + q];  // real: exact max|b|; complex: bound
+  if (cplx) {
+    bmax *= BOUND_SLACK;
+    if (!protect_update_is_one(p2(g - be) * bmax, hm0 + alam, arho, omega)) {
+      double m = 0.0;  // exact max |b| (rare: near overflow)
+      for (int r = 0; r < c.b_r; r++) {
+        double v = ghypot(c.X[col * c.ldx + r0 + r], c.X[(col + 1) * c.ldx + r0 + r]);
+        if (v > m) m = v;
+      }
+      bmax = m;
+    }
+  }
+  const int xe1 = protect_update_e(p2(g - be) * bmax, hm0 + alam, arho, omega);
+  int d = xe1 + g;
+  o.fb = p2(d - be);
+  o.fx = p2(d - ae);
+  o.rr = st.rho_re;
+  o.ri = st.rho_im;
+  if (o.fx != 1.0) {
+    o.rr = o.fx * o.rr;
+    o.ri = o.fx * o.ri;
+  }
+  o.zkr = st.zk_re;
+  o.zki = st.zk_im;
+  if (o.fx != 1.0) {
+    o.zkr *= o.fx;
+    o.zki *= o.fx;
+  }
+  o.x2 = 1.0;
+  // ---- step 2 (:255-278): bound of max|X'| = fb bmax + |rho| hmax0 + |lambda rho| ----
+  if (p.k > 1) {
+    const double zmax = o.fx != 1.0 ? o.fx * st.zmax : st.zmax;
+    const double rs = c.RS[(int64_t)jt * c.N + it];
+    const double arb = cplx ? fabs(o.rr) + fabs(o.ri) : fabs(o.rr);
+    const double alb = shifted ? fabs(lr) + fabs(li) : 0.0;
+    const double b1 = (o.fb * bmax + arb * hm0 + alb * arb) * BOUND_SLACK;
+    if (!protect_update_is_one(b1, rs, zmax, omega)) {
+      double m = 0.0;  // exact max |X'| (rare)
+      for (int r = 0; r < c.b_r; r++) {
+        const double h0 = c.H[(p.js - 1) * c.ldh + r0 + r];
+        const bool last = shifted && r == c.b_r - 1;
+        if (cplx) {
+          double xr = step1_apply(c.X[col * c.ldx + r0 + r], o.fb, o.rr, o.ri, h0, last, true,
+                                  false, lr, li);
+          double xi = step1_apply(c.X[(col + 1) * c.ldx + r0 + r], o.fb, o.rr, o.ri, h0, last,
+                                  true, true, lr, li);
+          double v = ghypot(xr, xi);
+          if (v > m) m = v;
+        } else {
+          double v = fabs(step1_apply(c.X[col * c.ldx + r0 + r], o.fb, o.rr, o.ri, h0, last,
+                                      false, false, lr, li));
+          if (v > m) m = v;
+        }
+      }
+      const int xe2 = protect_update_e(m, rs, zmax, omega);
+      if (xe2 < 0) {
+        o.x2 = p2(xe2);
+        d += xe2;
+        o.zkr *= o.x2;
+        o.zki *= o.x2;
+      }
+    }
+  }
+  o.dexp = d;
+  RSc[t] = o;
+}
+
+struct PanelSmem {
+  union {
+    struct {
+      double A[STAGES][BK][APAD];
+      double B[STAGES][2 * BN][BPAD];
+    } pipe;
+    double C[2 * BN][APAD];  // accumulators, [acc col][row]
+  } u;
+  RowScalars rsc[SMAX][BN / 2 * 2];  // per (segment, column): the column's shift record
+  unsigned long long red[2][SMAX][BN];
+  double x3[SMAX][BN], z3r[SMAX][BN], z3i[SMAX][BN];
+  int dex[SMAX][BN];
+  int need[SMAX][BN];
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void mma_f64(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// One K chunk of A (rows row0.., H columns js-1+kc*BK..) and of B.
+template <bool A16>
+__device__ __forceinline__ void panel_load(const Ctx& c, const PanelArgs& p, PanelSmem& sm,
+                                           int stage, int kc, int64_t row0, int rows_valid,
+                                           int64_t col0) {
+  const int tid = threadIdx.x;
+  if (A16) {
+#pragma unroll
+    for (int it = 0; it < (BK * BM / 2) / PANEL_THREADS; it++) {
+      int e = tid + it * PANEL_THREADS;
+      int kk = e / (BM / 2);
+      int m2 = (e % (BM / 2)) * 2;
+      int kglob = kc * BK + kk;
+      bool valid = kglob < p.k && m2 < rows_valid;
+      const double* src = c.H + (p.js - 1 + (valid ? kglob : 0)) * c.ldh + row0 + (valid ? m2 : 0);
+      cp_async16(&sm.u.pipe.A[stage][kk][m2], src, valid);
+    }
+  } else {
+#pragma unroll
+    for (int it = 0; it < (BK * BM) / PANEL_THREADS; it++) {
+      int e = tid + it * PANEL_THREADS;
+      int kk = e / BM;
+      int m = e % BM;
+      int kglob = kc * BK + kk;
+      bool valid = kglob < p.k && m < rows_valid;
+      const double* src = c.H + (p.js - 1 + (valid ? kglob : 0)) * c.ldh + row0 + (valid ? m : 0);
+      cp_async8(&sm.u.pipe.A[stage][kk][m], src, valid);
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < (2 * BN * BK / 2) / PANEL_THREADS; it++) {
+    int e = tid + it * PANEL_THREADS;
+    int nn = e / (BK / 2);
+    int k2 = (e % (BK / 2)) * 2;
+    const double* src = c.Bop + (2 * col0 + nn) * KP + kc * BK + k2;
+    cp_async16(&sm.u.pipe.B[stage][nn][k2], src, true);
+  }
+}
+
+// Epilogue mapping: thread -> column pair pc (CTA columns 2pc, 2pc+1; a
+// complex shift or two real shifts) and rows rp + 16 j.  For b_r % 16 == 0
+// (SEG16) the 16 threads of a pair share a segment for each j, so segment
+// maxima reduce with shuffles; otherwise through shared-memory atomics.
+constexpr int EP_ROWS = 16;                       // threads per column pair
+constexpr int EP_RPT = BM / EP_ROWS;              // rows per thread (8)
+
+template <bool SEG16>
+__device__ __forceinline__ void seg_max2(PanelSmem& sm, int slot, int sg, int cl0, double v0,
+                                         double v1, int rp) {
+  if (SEG16) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      double w0 = __shfl_xor_sync(0xffffffffu, v0, o);
+      double w1 = __shfl_xor_sync(0xffffffffu, v1, o);
+      v0 = w0 > v0 ? w0 : v0;
+      v1 = w1 > v1 ? w1 : v1;
+    }
+    if (rp == 0) {
+      unsigned long long* r = &sm.red[slot][sg][cl0];
+      if (dkey(v0) > r[0]) r[0] = dkey(v0);
+      if (dkey(v1) > r[1]) r[1] = dkey(v1);
+    }
+  } else {
+    atomicMax(&sm.red[slot][sg][cl0], dkey(v0));
+    atomicMax(&sm.red[slot][sg][cl0 + 1], dkey(v1));
+  }
+}
+
+template <bool A16, bool SEG16>
+__global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
+                                                            const RowScalars* __restrict__ RSc) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PanelSmem& sm = *reinterpret_cast<PanelSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int S = p.S;
+  const int tile0 = blockIdx.y * S;
+  const int ntiles = min(S, p.jt - tile0);
+  const int64_t row0 = (int64_t)tile0 * c.b_r;
+  const int rows_valid = ntiles * c.b_r;
+  const int64_t col0 = (int64_t)blockIdx.x * BN;
+  const int nk = (p.k + BK - 1) / BK;
+  const int jt = p.jt;
+  const double omega = c.omega;
+  const bool robust = c.robust;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; s++) {
+    if (s < nk) panel_load<A16>(c, p, sm, s, s, row0, rows_valid, col0);
+    cp_commit();
+  }
+  // per (segment, column) records of steps 1-2 (k_scalars) and red init
+  for (int e = tid; e < SMAX * BN; e += PANEL_THREADS) {
+    const int sg = e / BN, cc = e % BN;
+    const int64_t col = col0 + cc;
+    if (sg < ntiles && col < c.ncol) {
+      const int64_t q = col < 2 * c.mc ? col / 2 : c.mc + (col - 2 * c.mc);
+      sm.rsc[sg][cc] = RSc[(int64_t)(tile0 + sg) * c.ms + q];
+    }
+    sm.red[0][sg][cc] = 0ULL;
+    sm.red[1][sg][cc] = 0ULL;
+    sm.need[sg][cc] = 0;
+  }
+  // (ordered before the epilogue by the main loop's barriers)
+
+  // ---------------- main loop: acc = A [W | Zs] on DMMA ----------------
+  const int wm = warp & 3, wn = warp >> 2;
+  const int g = lane >> 2, t4 = lane & 3;
+  double acc[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
+
+  for (int kc = 0; kc < nk; kc++) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      int nxt = kc + STAGES - 1;
+      if (nxt < nk) panel_load<A16>(c, p, sm, nxt % STAGES, nxt, row0, rows_valid, col0);
+      cp_commit();
+    }
+    const int st = kc % STAGES;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[2][2], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++) {
+        int r = wm * 32 + mi * 16 + g;
+        af[mi][0] = sm.u.pipe.A[st][kk + t4][r];
+        af[mi][1] = sm.u.pipe.A[st][kk + t4][r + 8];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ni++) bf[ni] = sm.u.pipe.B[st][wn * 32 + ni * 8 + g][kk + t4];
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 4; ni++) mma_f64(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+    }
+  }
+  cp_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+    for (int ni = 0; ni < 4; ni++) {
+      int r = wm * 32 + mi * 16 + g;
+      int cc = wn * 32 + ni * 8 + 2 * t4;
+      sm.u.C[cc][r] = acc[mi][ni][0];
+      sm.u.C[cc + 1][r] = acc[mi][ni][1];
+      sm.u.C[cc][r + 8] = acc[mi][ni][2];
+      sm.u.C[cc + 1][r + 8] = acc[mi][ni][3];
+    }
+  __syncthreads();
+
+  // ---------------- epilogue ----------------
+  const int pc = tid / EP_ROWS, rp = tid % EP_ROWS;
+  const int cl0 = 2 * pc;                 // CTA-local columns cl0, cl0 + 1
+  const int64_t gc0 = col0 + cl0;         // global column of cl0
+  const bool cplx = gc0 < 2 * c.mc;
+  const bool v0 = gc0 < c.ncol, v1 = gc0 + 1 < c.ncol;
+  const int64_t q0 = cplx ? gc0 / 2 : c.mc + (gc0 - 2 * c.mc);
+  const int64_t q1 = cplx ? q0 : q0 + 1;
+  const double lr0 = v0 ? c.lam_re[q0] : 0.0, li0 = (v0 && cplx) ? c.lam_im[q0] : 0.0;
+  const double lr1 = v1 ? c.lam_re[q1] : 0.0;
+  // pass 1: X'' = x2 X' - (fx x2) (A Zs); bounds of max|X''|, max|Cr_old|
+  double xa[EP_RPT], xb[EP_RPT], ca[EP_RPT], cb[EP_RPT];
+  {
+    double mb0 = 0.0, mb1 = 0.0, mr0 = 0.0, mr1 = 0.0;
+    int seg = SEG16 ? 0 : -1;
+#pragma unroll
+    for (int j = 0; j < EP_RPT; j++) {
+      const int r = rp + EP_ROWS * j;
+      const bool ok = r < rows_valid;
+      const int sg = r / c.b_r;
+      double x0 = 0.0, x1 = 0.0, c0v = 0.0, c1v = 0.0;
+      if (ok) {
+        const int64_t grow = row0 + r;
+        const double h0 = c.H[(p.js - 1) * c.ldh + grow];
+        const bool last = ((r + 1) % c.b_r == 0) && (tile0 + sg == jt - 1);
+        if (v0) {
+          const RowScalars& s0 = sm.rsc[sg][cl0];
+          x0 = step1_apply(c.X[gc0 * c.ldx + grow], s0.fb, s0.rr, s0.ri, h0, last, cplx, false, lr0,
+                           li0);
+          if (s0.x2 < 1.0) x0 *= s0.x2;
+          x0 -= (s0.fx * s0.x2) * sm.u.C[2 * cl0 + 1][r];
+          c0v = c.Cr[gc0 * c.ldx + grow];
+        }
+        if (v1) {
+          const RowScalars& s1 = sm.rsc[sg][cl0 + 1];
+          x1 = step1_apply(c.X[(gc0 + 1) * c.ldx + grow], s1.fb, s1.rr, s1.ri, h0, last, cplx,
+                           true, cplx ? lr0 : lr1, li0);
+          if (s1.x2 < 1.0) x1 *= s1.x2;
+          x1 -= (s1.fx * s1.x2) * sm.u.C[2 * cl0 + 3][r];
+          c1v = c.Cr[(gc0 + 1) * c.ldx + grow];
+        }
+      }
+      xa[j] = x0;
+      xb[j] = x1;
+      ca[j] = c0v;
+      cb[j] = c1v;
+      double qb0, qb1, qr0, qr1;
+      if (cplx) {
+        qb0 = qb1 = fabs(x0) + fabs(x1);
+        qr0 = qr1 = fabs(c0v) + fabs(c1v);
+      } else {
+        qb0 = fabs(x0);
+        qb1 = fabs(x1);
+        qr0 = fabs(c0v);
+        qr1 = fabs(c1v);
+      }
+      if (SEG16) {
+        if (sg != seg) {  // uniform across the 16 threads of the pair
+          if (seg < ntiles) {
+            seg_max2<true>(sm, 0, seg, cl0, mb0, mb1, rp);
+            seg_max2<true>(sm, 1, seg, cl0, mr0, mr1, rp);
+          }
+          seg = sg;
+          mb0 = mb1 = mr0 = mr1 = 0.0;
+        }
+        mb0 = qb0 > mb0 ? qb0 : mb0;
+        mb1 = qb1 > mb1 ? qb1 : mb1;
+        mr0 = qr0 > mr0 ? qr0 : mr0;
+        mr1 = qr1 > mr1 ? qr1 : mr1;
+      } else if (ok) {
+        seg_max2<false>(sm, 0, sg, cl0, qb0, qb1, rp);
+        seg_max2<false>(sm, 1, sg, cl0, qr0, qr1, rp);
+      }
+    }
+    if (SEG16 && seg < ntiles) {
+      seg_max2<true>(sm, 0, seg, cl0, mb0, mb1, rp);
+      seg_max2<true>(sm, 1, seg, cl0, mr0, mr1, rp);
+    }
+  }
+  __syncthreads();
+  // step 3 guard (:287-301), one thread per (segment, column)
+  int my_need = 0;
+  for (int e = tid; e < SMAX * BN; e += PANEL_THREADS) {
+    const int sg = e / BN, cc = e % BN;
+    const int64_t col = col0 + cc;
+    if (sg >= ntiles || col >= c.ncol) continue;
+    const RowScalars& s = sm.rsc[sg][cc];
+    double zr = s.zkr, zi = s.zki;
+    double x3 = 1.0;
+    int dx = s.dexp;
+    if (robust) {
+      const double bb = dval(sm.red[0][sg][cc]), rb = dval(sm.red[1][sg][cc]);
+      if (col < 2 * c.mc) {
+        const double az = fabs(zr) + fabs(zi);
+        if (!protect_update_is_one(bb * BOUND_SLACK, rb * BOUND_SLACK, az * BOUND_SLACK, omega)) {
+          sm.need[sg][cc] = 1;
+          my_need = 1;
+        }
+      } else {
+        const int xe = protect_update_e(bb, rb, fabs(zr), omega);
+        if (xe < 0) {
+          x3 = p2(xe);
+          dx += xe;
+          zr *= x3;
+        }
+      }
+    }
+    sm.x3[sg][cc] = x3;
+    sm.z3r[sg][cc] = zr;
+    sm.z3i[sg][cc] = zi;
+    sm.dex[sg][cc] = dx;
+  }
+  if (__syncthreads_or(my_need)) {  // rare: exact hypot maxima for flagged complex columns
+    for (int e = tid; e < 2 * SMAX * BN; e += PANEL_THREADS) (&sm.red[0][0][0])[e] = 0ULL;
+    __syncthreads();
+    if (cplx && v0) {
+#pragma unroll
+      for (int j = 0; j < EP_RPT; j++) {
+        const int r = rp + EP_ROWS * j;
+        if (r < rows_valid) {
+          const int sg = r / c.b_r;
+          atomicMax(&sm.red[0][sg][cl0], dkey(ghypot(xa[j], xb[j])));
+          atomicMax(&sm.red[1][sg][cl0], dkey(ghypot(ca[j], cb[j])));
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < SMAX * BN; e += PANEL_THREADS) {
+      const int sg = e / BN, cc = e % BN;
+      if (!sm.need[sg][cc]) continue;
+      const int ccr = cc & ~1;  // the pair's maxima live in its re column
+      double zr = sm.z3r[sg][cc], zi = sm.z3i[sg][cc];
+      const int xe = protect_update_e(dval(sm.red[0][sg][ccr]), dval(sm.red[1][sg][ccr]),
+                                      ghypot(zr, zi), omega);
+      if (xe < 0) {
+        const double x3 = p2(xe);
+        sm.x3[sg][cc] = x3;
+        sm.dex[sg][cc] += xe;
+        sm.z3r[sg][cc] = zr * x3;
+        sm.z3i[sg][cc] = zi * x3;
+      }
+    }
+  }
+  for (int e = tid; e < SMAX * BN; e += PANEL_THREADS) (&sm.red[0][0][0])[e] = 0ULL;
+  __syncthreads();
+  // pass 2: X''' = x3 X'' - Cr_old zk ; Cr_new = A W + P Cr_old - c0 lambda e_{js-1}
+  {
+    const StepScalars st0 = c.SS[v0 ? q0 : 0];
+    const StepScalars st1 = c.SS[v1 ? q1 : 0];
+    double mb0 = 0.0, mb1 = 0.0;
+    int seg = SEG16 ? 0 : -1;
+#pragma unroll
+    for (int j = 0; j < EP_RPT; j++) {
+      const int r = rp + EP_ROWS * j;
+      const bool ok = r < rows_valid;
+      const int sg = r / c.b_r;
+      double x0 = xa[j], x1 = xb[j];
+      if (ok) {
+        const int64_t grow = row0 + r;
+        const bool lastrow = (grow == p.js - 1);
+        const double x30 = sm.x3[sg][cl0], x31 = sm.x3[sg][cl0 + 1];
+        if (x30 < 1.0) x0 *= x30;
+        if (x31 < 1.0) x1 *= x31;
+        double n0, n1;
+        if (cplx) {
+          const double zr = sm.z3r[sg][cl0], zi = sm.z3i[sg][cl0];
+          const double zr1 = sm.z3r[sg][cl0 + 1], zi1 = sm.z3i[sg][cl0 + 1];
+          x0 -= ca[j] * zr - cb[j] * zi;
+          x1 -= ca[j] * zi1 + cb[j] * zr1;
+          n0 = sm.u.C[2 * cl0][r] + st0.P * ca[j];
+          n1 = sm.u.C[2 * cl0 + 2][r] + st0.P * cb[j];
+          if (lastrow) {
+            n0 -= st0.c0_re * lr0 - st0.c0_im * li0;
+            n1 -= st0.c0_re * li0 + st0.c0_im * lr0;
+          }
+        } else {
+          x0 -= ca[j] * sm.z3r[sg][cl0];
+          x1 -= cb[j] * sm.z3r[sg][cl0 + 1];
+          n0 = sm.u.C[2 * cl0][r] + st0.P * ca[j];
+          n1 = sm.u.C[2 * cl0 + 2][r] + st1.P * cb[j];
+          if (lastrow) {
+            n0 -= st0.c0_re * lr0;
+            n1 -= st1.c0_re * lr1;
+          }
+        }
+        if (v0) {
+          c.X[gc0 * c.ldx + grow] = x0;
+          c.Cr[gc0 * c.ldx + grow] = n0;
+        }
+        if (v1) {
+          c.X[(gc0 + 1) * c.ldx + grow] = x1;
+          c.Cr[(gc0 + 1) * c.ldx + grow] = n1;
+        }
+      }
+      double qb0, qb1;
+      if (cplx) {
+        qb0 = qb1 = fabs(x0) + fabs(x1);
+      } else {
+        qb0 = fabs(x0);
+        qb1 = fabs(x1);
+      }
+      if (SEG16) {
+        if (sg != seg) {
+          if (seg < ntiles) seg_max2<true>(sm, 0, seg, cl0, mb0, mb1, rp);
+          seg = sg;
+          mb0 = mb1 = 0.0;
+        }
+        if (ok) {
+          mb0 = qb0 > mb0 ? qb0 : mb0;
+          mb1 = qb1 > mb1 ? qb1 : mb1;
+        }
+      } else if (ok) {
+        seg_max2<false>(sm, 0, sg, cl0, qb0, qb1, rp);
+      }
+    }
+    if (SEG16 && seg < ntiles) seg_max2<true>(sm, 0, seg, cl0, mb0, mb1, rp);
+  }
+  __syncthreads();
+  // new beta and the step-1 bound for the next tile column
+  for (int e = tid; e < SMAX * BN; e += PANEL_THREADS) {
+    const int sg = e / BN, cc = e % BN;
+    const int64_t col = col0 + cc;
+    if (sg >= ntiles || col >= c.ncol) continue;
+    const bool cx = col < 2 * c.mc;
+    if (cx && (col & 1)) continue;
+    const int64_t q = cx ? col / 2 : c.mc + (col - 2 * c.mc);
+    const int64_t ix = (int64_t)(tile0 + sg) * c.ms + q;
+    if (robust) c.E[ix] = sm.dex[sg][cc];
+    c.XB[ix] = dval(sm.red[0][sg][cc]);
+  }
+}
