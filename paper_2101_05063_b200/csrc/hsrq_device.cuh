@@ -54,7 +54,7 @@ __device__ __forceinline__ double hypot_kernel(double ax, double ay) {
   return h;
 }
 
-__device__ __noinline__ double ghypot(double x, double y) {
+__device__ __forceinline__ double ghypot(double x, double y) {
   if (!isfinite(x) || !isfinite(y)) {
     if (isinf(x) || isinf(y)) return __longlong_as_double(0x7ff0000000000000LL);
     return x + y;
@@ -103,7 +103,7 @@ __device__ __forceinline__ int pow2floor_e(double x) {
 
 // protect_update (numba_backend.py:47-67); returns log2(xi): 0 when xi == 1,
 // EXP_ZERO when the halving loop reached 0.
-__device__ __noinline__ int protect_update_e(double bnorm, double hnorm, double xnorm,
+__device__ __forceinline__ int protect_update_e(double bnorm, double hnorm, double xnorm,
                                              double omega) {
   double cand;
   if (xnorm <= 1.0) {

@@ -41,8 +41,6 @@ using namespace hsrq;
 namespace {
 
 constexpr int MAXK = 128;    // largest tile (b_r) supported on the GPU path
-constexpr int SLOTS = 4;     // rows per lane in the diagonal kernel (MAXK / 32)
-constexpr int DIAG_WARPS = 8;
 
 // Panel GEMM tiling.
 constexpr int BM = 128;      // rows per CTA (whole tile rows)
@@ -79,6 +77,7 @@ struct Ctx {
   StepScalars* SS;       // ms
   double* HM0;           // N x N : max |H[tile i rows, js-1]|
   double* RS;            // N x N : max row sum |H[tile i rows, js:je-1]|
+  double* HMK;           // N x MAXK : max_{i<kp} |h(i, kp-1)| of each diagonal tile
   double* XB;            // N x ms: max |X| over each tile's rows (real: exact;
                          // complex: max(|re|+|im|), an upper bound of max |x|)
   int64_t* fail;         // ms
@@ -117,6 +116,20 @@ __global__ void k_tables(Ctx c) {
   for (int j = 1; j < k; j++) acc += fabs(c.H[(js - 1 + j) * c.ldh + r]);
   atomicMax((unsigned long long*)&c.HM0[(int64_t)jt * c.N + i], dkey(h0));
   atomicMax((unsigned long long*)&c.RS[(int64_t)jt * c.N + i], dkey(acc));
+}
+
+// HMK[jt][kp] = max_{i<kp} |H[js+i, js+kp-1]| (the hmax of solve_rsolve :155-163).
+__global__ void k_hmk(Ctx c) {
+  const int jt = blockIdx.x, kp = threadIdx.x;
+  const int64_t js = (int64_t)jt * c.b_r;
+  const int64_t je = js + c.b_r < c.n ? js + c.b_r : c.n;
+  if (kp < 1 || kp >= (int)(je - js)) return;
+  double m = 0.0;
+  for (int i = 0; i < kp; i++) {
+    const double v = fabs(c.H[(js + kp - 1) * c.ldh + js + i]);
+    if (v > m) m = v;
+  }
+  c.HMK[(int64_t)jt * MAXK + kp] = m;
 }
 
 // X = B (or the broadcast start vector), Cr(:, N-1) = H(:, n-1) - lambda e_n
@@ -160,592 +173,7 @@ __global__ void k_zero_bop(double* Bop, int64_t count) {
   if (t < count) Bop[t] = 0.0;
 }
 
-// ---------------------------------------------------------------------------
-// k_diag: diagonal tile (one warp per shift)
-// ---------------------------------------------------------------------------
-
-template <typename T>
-__device__ __forceinline__ T sel(const T (&a)[SLOTS], int j) {
-  T r = a[0];
-#pragma unroll
-  for (int t = 1; t < SLOTS; t++)
-    if (j == t) r = a[t];
-  return r;
-}
-template <typename T>
-__device__ __forceinline__ void put(T (&a)[SLOTS], int j, T v) {
-#pragma unroll
-  for (int t = 0; t < SLOTS; t++)
-    if (j == t) a[t] = v;
-}
-
-struct DiagSmem {
-  double hs[MAXK * (MAXK + 1) / 2 + MAXK];  // packed tile columns 0..k-2, rows 0..t+1
-  double hmax[MAXK];                        // max_{i<kp} |h(i, kp-1)|
-  double cs_c[DIAG_WARPS][MAXK];
-  double cs_ci[DIAG_WARPS][MAXK];
-  double cs_s[DIAG_WARPS][MAXK];
-};
-
-__device__ __forceinline__ int hs_off(int t) { return t * (t + 3) / 2; }
-
-struct DiagArgs {
-  int jt;
-  int64_t js;
-  int k;
-  int has_left;
-  // tile-level mode (hsrq_tile_diag): explicit tile buffers instead of the sweep state
-  int tile_mode;
-  const double* t_hdiag;   // k x (k-1) row-major
-  const double* t_hleft;
-  const double* t_rright;  // k x b / 2b row-major
-  double* t_x;
-  double *t_cre, *t_cim, *t_s;
-  int32_t* t_beta;
-  int64_t* t_status;
-  int t_b;
-};
-
-__device__ __forceinline__ void record_fail(const Ctx& c, int64_t q, int phase, int tile, int row,
-                                            const DiagArgs& a) {
-  if (a.tile_mode) {
-    a.t_status[q] = (int64_t)(phase) * (1LL << 42) + (int64_t)row;
-    return;
-  }
-  if (c.fail[q] == 0) {
-    c.fail[q] = pack_fail(phase, tile, row);
-    atomicAdd(c.nfail, 1ULL);
-  }
-}
-
-// Real shift: reduce_diag + solve_rsolve fused (same v recurrence, identical
-// arithmetic), then the panel operands.
-__device__ void diag_real(const Ctx& c, const DiagArgs& a, DiagSmem& sm, int64_t q, int64_t col,
-                          int warp, double hleft0) {
-  const int lane = threadIdx.x & 31;
-  const int k = a.k;
-  const double lam = c.lam_re[q];
-  const double omega = c.omega;
-  const bool robust = c.robust;
-  double v[SLOTS], x[SLOTS];
-#pragma unroll
-  for (int j = 0; j < SLOTS; j++) {
-    int i = lane + 32 * j;
-    if (i < k) {
-      if (a.tile_mode) {
-        v[j] = a.t_rright[(int64_t)i * a.t_b + q];
-        x[j] = a.t_x[(int64_t)i * a.t_b + q];
-      } else {
-        v[j] = c.Cr[col * c.ldx + a.js + i];
-        x[j] = c.X[col * c.ldx + a.js + i];
-      }
-    } else {
-      v[j] = 0.0;
-      x[j] = 0.0;
-    }
-  }
-  double* csc = sm.cs_c[warp];
-  double* css = sm.cs_s[warp];
-  int gexp = 0;
-  bool failed = false;
-  for (int kp = k - 1; kp >= 1; --kp) {
-    const int o = kp & 31, sl = kp >> 5;
-    double vk = __shfl_sync(0xffffffffu, sel(v, sl), o);
-    double xk = __shfl_sync(0xffffffffu, sel(x, sl), o);
-    const double* hcol = sm.hs + hs_off(kp - 1);
-    const double av = hcol[kp];
-    double r = ghypot(av, vk);
-    if (r == 0.0) {
-      if (lane == 0) record_fail(c, q, HSRQ_KIND_DEGENERATE, a.jt, kp, a);
-      failed = true;
-      break;
-    }
-    const double cc = vk / r, ss = -av / r;
-    if (lane == 0) {
-      csc[kp] = cc;
-      css[kp] = ss;
-    }
-    const double phi = vk * cc - av * ss;
-    if (phi == 0.0) {
-      if (lane == 0) record_fail(c, q, HSRQ_KIND_SINGULAR, a.jt, kp, a);
-      failed = true;
-      break;
-    }
-    if (robust) {
-      double aphi = fabs(phi), ax = fabs(xk);
-      if (aphi < 1.0 && ax > aphi * omega) {
-        int e = pow2floor_e(aphi * omega / ax);
-        double xi = p2(e);
-#pragma unroll
-        for (int j = 0; j < SLOTS; j++) x[j] *= xi;
-        xk *= xi;
-        gexp += e;
-      }
-    }
-    xk = xk / phi;
-    if (robust) {
-      double xm = 0.0, vm = 0.0;
-#pragma unroll
-      for (int j = 0; j < SLOTS; j++) {
-        int i = lane + 32 * j;
-        if (i < kp) {
-          double ax = fabs(x[j]), avv = fabs(v[j]);
-          if (ax > xm) xm = ax;
-          if (avv > vm) vm = avv;
-        }
-      }
-      xm = warp_max(xm);
-      vm = warp_max(vm);
-      int e = protect_update_e(xm, vm + sm.hmax[kp] + fabs(lam), fabs(xk), omega);
-      if (e < 0) {
-        double xi = p2(e);
-#pragma unroll
-        for (int j = 0; j < SLOTS; j++) x[j] *= xi;
-        xk *= xi;
-        gexp += e;
-      }
-    }
-    if (lane == o) put(x, sl, xk);
-    const double tau1 = ss * xk, tau2 = cc * xk;
-#pragma unroll
-    for (int j = 0; j < SLOTS; j++) {
-      int i = lane + 32 * j;
-      if (i < kp - 1) {
-        double hi = hcol[i];
-        x[j] = (x[j] - tau2 * v[j]) + tau1 * hi;
-        v[j] = cc * hi + ss * v[j];
-      } else if (i == kp - 1) {
-        double hd = hcol[i] - lam;
-        x[j] = (x[j] - tau2 * v[j]) + tau1 * hd;
-        v[j] = cc * hd + ss * v[j];
-      }
-    }
-  }
-  if (failed) return;
-  // cross-tile rotation (reduce_diag :94-105) and the last pivot (:178-192)
-  double v0 = __shfl_sync(0xffffffffu, v[0], 0);
-  double x0 = __shfl_sync(0xffffffffu, x[0], 0);
-  double c0 = 1.0, s0 = 0.0, piv = v0;
-  if (a.has_left) {
-    double al = hleft0;
-    double r = ghypot(al, v0);
-    if (r == 0.0) {
-      if (lane == 0) record_fail(c, q, HSRQ_KIND_DEGENERATE, a.jt, 0, a);
-      return;
-    }
-    c0 = v0 / r;
-    s0 = -al / r;
-    piv = v0 * c0 - al * s0;
-  }
-  if (lane == 0) {
-    csc[0] = c0;
-    css[0] = s0;
-  }
-  if (piv == 0.0) {
-    if (lane == 0) record_fail(c, q, HSRQ_KIND_SINGULAR, a.jt, 0, a);
-    return;
-  }
-  if (robust) {
-    double avv = fabs(piv), ax = fabs(x0);
-    if (avv < 1.0 && ax > avv * omega) {
-      int e = pow2floor_e(avv * omega / ax);
-      double xi = p2(e);
-#pragma unroll
-      for (int j = 0; j < SLOTS; j++) x[j] *= xi;
-      x0 *= xi;
-      gexp += e;
-    }
-  }
-  x0 = x0 / piv;
-  if (lane == 0) x[0] = x0;
-  __syncwarp();
-
-  // outputs: solution tile, rotations, scale exponent
-#pragma unroll
-  for (int j = 0; j < SLOTS; j++) {
-    int i = lane + 32 * j;
-    if (i < k) {
-      if (a.tile_mode) {
-        a.t_x[(int64_t)i * a.t_b + q] = x[j];
-        a.t_cre[(int64_t)i * a.t_b + q] = csc[i];
-        a.t_s[(int64_t)i * a.t_b + q] = css[i];
-        if (a.t_cim) a.t_cim[(int64_t)i * a.t_b + q] = 0.0;
-      } else {
-        c.X[col * c.ldx + a.js + i] = x[j];
-        c.c_re[q * c.ldc + a.js + i] = csc[i];
-        c.s[q * c.ldc + a.js + i] = css[i];
-        if (c.c_im) c.c_im[q * c.ldc + a.js + i] = 0.0;
-      }
-    }
-  }
-  if (a.tile_mode) {
-    if (lane == 0) a.t_beta[q] += gexp;
-    return;
-  }
-  if (lane == 0) c.E[(int64_t)a.jt * c.ms + q] += gexp;
-  if (a.jt == 0) return;
-
-  // ---- panel operands ----
-  // W_j = c_j prod_{t<j} s_t, P = prod_t s_t; Z: update_rupdate :246-253.
-  double w[SLOTS], z[SLOTS];
-#pragma unroll
-  for (int j = 0; j < SLOTS; j++) w[j] = z[j] = 0.0;
-  double pre = 1.0;
-  double carry = c0 * __shfl_sync(0xffffffffu, x[0], 0);  // Z[0] = c[0] * Z[0]
-  for (int j = 0; j < k; j++) {
-    const double cj = csc[j], sj = css[j];
-    const int oj = j & 31, slj = j >> 5;
-    if (lane == oj) put(w, slj, cj * pre);
-    pre = pre * sj;
-    if (j >= 1) {
-      double t2 = __shfl_sync(0xffffffffu, sel(x, slj), oj);
-      double t1 = carry;
-      double zf = cj * t1 - sj * t2;  // final Z[j-1]
-      carry = sj * t1 + cj * t2;
-      const int om = (j - 1) & 31, slm = (j - 1) >> 5;
-      if (lane == om) put(z, slm, zf);
-    }
-  }
-  // zmax over Z[0:k-1]
-  double zm = 0.0;
-#pragma unroll
-  for (int j = 0; j < SLOTS; j++) {
-    int i = lane + 32 * j;
-    if (i < k - 1 && fabs(z[j]) > zm) zm = fabs(z[j]);
-  }
-  zm = warp_max(zm);
-  // B operand: column 2*col = W, 2*col+1 = [0, Z[0..k-2]]
-  double* bw = c.Bop + (2 * col) * KP;
-  double* bz = c.Bop + (2 * col + 1) * KP;
-#pragma unroll
-  for (int j = 0; j < SLOTS; j++) {
-    int i = lane + 32 * j;
-    if (i < KP) {
-      bw[i] = i < k ? w[j] : 0.0;
-      // Zs[i+1] = Z[i]
-      if (i + 1 < KP) bz[i + 1] = (i < k - 1) ? z[j] : 0.0;
-    }
-  }
-  if (lane == 0) {
-    bz[0] = 0.0;
-    StepScalars st;
-    st.rho_re = s0 * x0;
-    st.rho_im = 0.0;
-    st.zk_re = carry;
-    st.zk_im = 0.0;
-    st.zmax = zm;
-    st.P = pre;
-    st.c0_re = c0;
-    st.c0_im = 0.0;
-    c.SS[q] = st;
-  }
-}
-
-// Complex shift: creduce_diag + _build_complex_r + robust_trsv_complex,
-// with R's column kp formed and consumed at step kp.
-__device__ void diag_cplx(const Ctx& c, const DiagArgs& a, DiagSmem& sm, int64_t q, int64_t col,
-                          int warp, double hleft0) {
-  const int lane = threadIdx.x & 31;
-  const int k = a.k;
-  const double lre = c.lam_re[q], lim = c.lam_im[q];
-  const double omega = c.omega;
-  const bool robust = c.robust;
-  cplx v[SLOTS], x[SLOTS];
-#pragma unroll
-  for (int j = 0; j < SLOTS; j++) {
-    int i = lane + 32 * j;
-    if (i < k) {
-      if (a.tile_mode) {
-        int64_t b2 = 2 * (int64_t)a.t_b;
-        v[j] = mk(a.t_rright[i * b2 + 2 * q], a.t_rright[i * b2 + 2 * q + 1]);
-        x[j] = mk(a.t_x[i * b2 + 2 * q], a.t_x[i * b2 + 2 * q + 1]);
-      } else {
-        v[j] = mk(c.Cr[col * c.ldx + a.js + i], c.Cr[(col + 1) * c.ldx + a.js + i]);
-        x[j] = mk(c.X[col * c.ldx + a.js + i], c.X[(col + 1) * c.ldx + a.js + i]);
-      }
-    } else {
-      v[j] = mk(0.0, 0.0);
-      x[j] = mk(0.0, 0.0);
-    }
-  }
-  double* csc = sm.cs_c[warp];
-  double* csi = sm.cs_ci[warp];
-  double* css = sm.cs_s[warp];
-  int gexp = 0;
-  for (int kp = k - 1; kp >= 1; --kp) {
-    const int o = kp & 31, sl = kp >> 5;
-    cplx vsel = sel(v, sl), xsel = sel(x, sl);
-    cplx vk = mk(__shfl_sync(0xffffffffu, vsel.re, o), __shfl_sync(0xffffffffu, vsel.im, o));
-    cplx xk = mk(__shfl_sync(0xffffffffu, xsel.re, o), __shfl_sync(0xffffffffu, xsel.im, o));
-    const double* hcol = sm.hs + hs_off(kp - 1);
-    const double av = hcol[kp];
-    double absv = ghypot(vk.re, vk.im);
-    double r = ghypot(av, absv);
-    if (r == 0.0) {
-      if (lane == 0) record_fail(c, q, HSRQ_KIND_DEGENERATE, a.jt, kp, a);
-      return;
-    }
-    const double cr = vk.re / r, ci = vk.im / r, sv = -av / r;
-    if (lane == 0) {
-      csc[kp] = cr;
-      csi[kp] = ci;
-      css[kp] = sv;
-    }
-    const cplx cc = mk(cr, ci), ccj = mk(cr, -ci), svc = mk(sv, 0.0);
-    // R column kp: r_i = conj(c) v_i - s t_i  (i <= kp)
-    cplx rcol[SLOTS];
-#pragma unroll
-    for (int j = 0; j < SLOTS; j++) {
-      int i = lane + 32 * j;
-      cplx t = mk(i <= kp ? hcol[i] : 0.0, 0.0);
-      if (i == kp - 1) t = csub(t, mk(lre, lim));
-      rcol[j] = csub(cmul(ccj, v[j]), cmul(svc, t));
-    }
-    const cplx d = csub(cmul(ccj, vk), cmul(svc, mk(av, 0.0)));
-    if (d.re == 0.0 && d.im == 0.0) {
-      if (lane == 0) record_fail(c, q, HSRQ_KIND_SINGULAR, a.jt, kp, a);
-      return;
-    }
-    if (robust) {
-      double ad = cabs_(d), ax = cabs_(xk);
-      if (ad < 1.0 && ax > ad * omega) {
-        int e = pow2floor_e(ad * omega / ax);
-        cplx xi = mk(p2(e), 0.0);
-#pragma unroll
-        for (int j = 0; j < SLOTS; j++) x[j] = cmul(x[j], xi);
-        xk = cmul(xk, xi);
-        gexp += e;
-      }
-    }
-    xk = cdiv(xk, d);
-    if (robust) {
-      // upper bounds first (|z| <= (|re|+|im|)(1+2^-50)); exact hypots only if needed
-      double rb = 0.0, bb = 0.0;
-#pragma unroll
-      for (int j = 0; j < SLOTS; j++) {
-        int i = lane + 32 * j;
-        if (i < kp) {
-          double q1 = fabs(rcol[j].re) + fabs(rcol[j].im);
-          double q2 = fabs(x[j].re) + fabs(x[j].im);
-          if (q1 > rb) rb = q1;
-          if (q2 > bb) bb = q2;
-        }
-      }
-      rb = warp_max(rb) * (1.0 + 0x1p-50);
-      bb = warp_max(bb) * (1.0 + 0x1p-50);
-      double axk = cabs_(xk);
-      if (!protect_update_is_one(bb, rb, axk, omega)) {
-        double rm = 0.0, bm = 0.0;
-#pragma unroll
-        for (int j = 0; j < SLOTS; j++) {
-          int i = lane + 32 * j;
-          if (i < kp) {
-            double q1 = cabs_(rcol[j]), q2 = cabs_(x[j]);
-            if (q1 > rm) rm = q1;
-            if (q2 > bm) bm = q2;
-          }
-        }
-        rm = warp_max(rm);
-        bm = warp_max(bm);
-        int e = protect_update_e(bm, rm, axk, omega);
-        if (e < 0) {
-          cplx xi = mk(p2(e), 0.0);
-#pragma unroll
-          for (int j = 0; j < SLOTS; j++) x[j] = cmul(x[j], xi);
-          xk = cmul(xk, xi);
-          gexp += e;
-        }
-      }
-    }
-    if (lane == o) put(x, sl, xk);
-#pragma unroll
-    for (int j = 0; j < SLOTS; j++) {
-      int i = lane + 32 * j;
-      if (i < kp) {
-        x[j] = csub(x[j], cmul(xk, rcol[j]));
-        if (i < kp - 1) {
-          double hi = hcol[i];
-          v[j] = mk(cr * hi + sv * v[j].re, ci * hi + sv * v[j].im);
-        } else {
-          double tre = hcol[i] - lre, tim = -lim;
-          v[j] = mk((cr * tre - ci * tim) + sv * v[j].re, (cr * tim + ci * tre) + sv * v[j].im);
-        }
-      }
-    }
-  }
-  // j = 0: cross-tile rotation (creduce_diag :449-463) and R[0,0] (:546-550)
-  cplx v0 = mk(__shfl_sync(0xffffffffu, v[0].re, 0), __shfl_sync(0xffffffffu, v[0].im, 0));
-  cplx x0 = mk(__shfl_sync(0xffffffffu, x[0].re, 0), __shfl_sync(0xffffffffu, x[0].im, 0));
-  double c0r = 1.0, c0i = 0.0, s0 = 0.0;
-  cplx d = v0;
-  if (a.has_left) {
-    double al = hleft0;
-    double absv = ghypot(v0.re, v0.im);
-    double r = ghypot(al, absv);
-    if (r == 0.0) {
-      if (lane == 0) record_fail(c, q, HSRQ_KIND_DEGENERATE, a.jt, 0, a);
-      return;
-    }
-    c0r = v0.re / r;
-    c0i = v0.im / r;
-    s0 = -al / r;
-    d = csub(cmul(mk(c0r, -c0i), v0), cmul(mk(s0, 0.0), mk(al, 0.0)));
-  }
-  if (lane == 0) {
-    csc[0] = c0r;
-    csi[0] = c0i;
-    css[0] = s0;
-  }
-  if (d.re == 0.0 && d.im == 0.0) {
-    if (lane == 0) record_fail(c, q, HSRQ_KIND_SINGULAR, a.jt, 0, a);
-    return;
-  }
-  if (robust) {
-    double ad = cabs_(d), ax = cabs_(x0);
-    if (ad < 1.0 && ax > ad * omega) {
-      int e = pow2floor_e(ad * omega / ax);
-      cplx xi = mk(p2(e), 0.0);
-#pragma unroll
-      for (int j = 0; j < SLOTS; j++) x[j] = cmul(x[j], xi);
-      x0 = cmul(x0, xi);
-      gexp += e;
-    }
-  }
-  x0 = cdiv(x0, d);
-  if (lane == 0) x[0] = x0;
-  __syncwarp();
-
-#pragma unroll
-  for (int j = 0; j < SLOTS; j++) {
-    int i = lane + 32 * j;
-    if (i < k) {
-      if (a.tile_mode) {
-        int64_t b2 = 2 * (int64_t)a.t_b;
-        a.t_x[i * b2 + 2 * q] = x[j].re;
-        a.t_x[i * b2 + 2 * q + 1] = x[j].im;
-        a.t_cre[(int64_t)i * a.t_b + q] = csc[i];
-        a.t_cim[(int64_t)i * a.t_b + q] = csi[i];
-        a.t_s[(int64_t)i * a.t_b + q] = css[i];
-      } else {
-        c.X[col * c.ldx + a.js + i] = x[j].re;
-        c.X[(col + 1) * c.ldx + a.js + i] = x[j].im;
-        c.c_re[q * c.ldc + a.js + i] = csc[i];
-        c.c_im[q * c.ldc + a.js + i] = csi[i];
-        c.s[q * c.ldc + a.js + i] = css[i];
-      }
-    }
-  }
-  if (a.tile_mode) {
-    if (lane == 0) a.t_beta[q] += gexp;
-    return;
-  }
-  if (lane == 0) c.E[(int64_t)a.jt * c.ms + q] += gexp;
-  if (a.jt == 0) return;
-
-  // ---- panel operands (cupdate_crupdate :645-666; W complex, P real) ----
-  cplx w[SLOTS], z[SLOTS];
-#pragma unroll
-  for (int j = 0; j < SLOTS; j++) w[j] = z[j] = mk(0.0, 0.0);
-  double pre = 1.0;
-  cplx carry = mk(c0r * x0.re + c0i * x0.im, c0r * x0.im - c0i * x0.re);
-  for (int j = 0; j < k; j++) {
-    const double cr = csc[j], ci = csi[j], sj = css[j];
-    const int oj = j & 31, slj = j >> 5;
-    if (lane == oj) put(w, slj, mk(cr * pre, ci * pre));
-    pre = pre * sj;
-    if (j >= 1) {
-      cplx xs = sel(x, slj);
-      cplx t2 = mk(__shfl_sync(0xffffffffu, xs.re, oj), __shfl_sync(0xffffffffu, xs.im, oj));
-      cplx t1 = carry;
-      cplx zf = mk((cr * t1.re - ci * t1.im) - sj * t2.re, (cr * t1.im + ci * t1.re) - sj * t2.im);
-      carry = mk(sj * t1.re + (cr * t2.re + ci * t2.im), sj * t1.im + (cr * t2.im - ci * t2.re));
-      const int om = (j - 1) & 31, slm = (j - 1) >> 5;
-      if (lane == om) put(z, slm, zf);
-    }
-  }
-  double zm = 0.0;
-#pragma unroll
-  for (int j = 0; j < SLOTS; j++) {
-    int i = lane + 32 * j;
-    if (i < k - 1) {
-      double qz = cabs_(z[j]);
-      if (qz > zm) zm = qz;
-    }
-  }
-  zm = warp_max(zm);
-  double* bw_re = c.Bop + (2 * col) * KP;
-  double* bz_re = c.Bop + (2 * col + 1) * KP;
-  double* bw_im = c.Bop + (2 * (col + 1)) * KP;
-  double* bz_im = c.Bop + (2 * (col + 1) + 1) * KP;
-#pragma unroll
-  for (int j = 0; j < SLOTS; j++) {
-    int i = lane + 32 * j;
-    if (i < KP) {
-      bw_re[i] = i < k ? w[j].re : 0.0;
-      bw_im[i] = i < k ? w[j].im : 0.0;
-      if (i + 1 < KP) {
-        bz_re[i + 1] = (i < k - 1) ? z[j].re : 0.0;
-        bz_im[i + 1] = (i < k - 1) ? z[j].im : 0.0;
-      }
-    }
-  }
-  if (lane == 0) {
-    bz_re[0] = 0.0;
-    bz_im[0] = 0.0;
-    StepScalars st;
-    st.rho_re = s0 * x0.re;
-    st.rho_im = s0 * x0.im;
-    st.zk_re = carry.re;
-    st.zk_im = carry.im;
-    st.zmax = zm;
-    st.P = pre;
-    st.c0_re = c0r;
-    st.c0_im = c0i;
-    c.SS[q] = st;
-  }
-}
-
-__global__ void __launch_bounds__(DIAG_WARPS * 32) k_diag(Ctx c, DiagArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  DiagSmem& sm = *reinterpret_cast<DiagSmem*>(smem_raw);
-  const int k = a.k;
-  // stage the diagonal tile (columns 0..k-2, rows 0..t+1) and per-kp maxima
-  for (int t = 0; t + 1 < k; t++) {
-    for (int i = threadIdx.x; i <= t + 1; i += blockDim.x) {
-      double h = a.tile_mode ? a.t_hdiag[(int64_t)i * (k - 1) + t]
-                             : c.H[(a.js + t) * c.ldh + a.js + i];
-      sm.hs[hs_off(t) + i] = h;
-    }
-  }
-  __syncthreads();
-  for (int kp = 1 + threadIdx.x; kp < k; kp += blockDim.x) {
-    const double* hcol = sm.hs + hs_off(kp - 1);
-    double m = 0.0;
-    for (int i = 0; i < kp; i++)
-      if (fabs(hcol[i]) > m) m = fabs(hcol[i]);
-    sm.hmax[kp] = m;
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5;
-  const int64_t q = (int64_t)blockIdx.x * DIAG_WARPS + warp;
-  const int64_t ms = a.tile_mode ? a.t_b : c.ms;
-  if (q >= ms) return;
-  bool cplx;
-  int64_t col;
-  if (a.tile_mode) {
-    cplx = c.mc != 0;
-    col = 0;
-  } else {
-    col_of_shift(c, q, cplx, col);
-    if (c.fail[q] != 0) return;
-  }
-  double hleft0 = 0.0;
-  if (a.has_left) hleft0 = a.tile_mode ? a.t_hleft[0] : c.H[(a.js - 1) * c.ldh + a.js];
-  if (cplx)
-    diag_cplx(c, a, sm, q, col, warp, hleft0);
-  else
-    diag_real(c, a, sm, q, col, warp, hleft0);
-}
+#include "hsrq_diag.cuh"
 
 #include "hsrq_panel.cuh"
 
@@ -785,7 +213,7 @@ bool ck(cudaError_t e, const char* what) {
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t cr, bop, ss, hm0, rs, xb, rsc, nfail, total;
+  size_t cr, bop, ss, hm0, rs, hmk, xb, rsc, nfail, total;
 };
 
 WsLayout ws_layout(int64_t n, int b_r, int64_t mc, int64_t mr) {
@@ -807,6 +235,8 @@ WsLayout ws_layout(int64_t n, int b_r, int64_t mc, int64_t mr) {
   off = align_up(off + sizeof(double) * (size_t)N * N, 256);
   L.rs = off;
   off = align_up(off + sizeof(double) * (size_t)N * N, 256);
+  L.hmk = off;
+  off = align_up(off + sizeof(double) * (size_t)N * MAXK, 256);
   L.xb = off;
   off = align_up(off + sizeof(double) * (size_t)N * ms, 256);
   L.rsc = off;
@@ -856,6 +286,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   c.HM0 = (double*)(w + L.hm0);
   c.RS = (double*)(w + L.rs);
   c.XB = (double*)(w + L.xb);
+  c.HMK = (double*)(w + L.hmk);
   c.fail = fail;
   c.nfail = (unsigned long long*)(w + L.nfail);
   c.robust = robust;
@@ -869,11 +300,14 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   }
 
   static bool attr_done = false;
-  const size_t diag_smem = sizeof(DiagSmem);
+  const size_t dsm_r = sizeof(double) * (MAXK + DWR * (2 * MAXK * DG + 2 * MAXK));
+  const size_t dsm_c = sizeof(double) * (MAXK + DWC * (4 * MAXK * DG + 2 * MAXK));
   const size_t panel_smem = sizeof(PanelSmem);
   if (!attr_done) {
-    if (!ck(cudaFuncSetAttribute(k_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem),
+    if (!ck(cudaFuncSetAttribute(k_diag_real, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_r),
             "attr diag") ||
+        !ck(cudaFuncSetAttribute(k_diag_cplx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_c),
+            "attr diagc") ||
         !ck(cudaFuncSetAttribute(k_panel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)panel_smem), "attr panel") ||
         !ck(cudaFuncSetAttribute(k_panel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -904,6 +338,8 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     k_tables<<<gt, 256, 0, stream>>>(c);
     g_launches++;
   }
+  k_hmk<<<(unsigned)c.N, MAXK, 0, stream>>>(c);
+  g_launches++;
   {
     dim3 gi((unsigned)((n + 255) / 256), (unsigned)c.ncol);
     k_init<<<gi, 256, 0, stream>>>(c, B, ldb, b_broadcast);
@@ -920,9 +356,20 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     int64_t je = a.js + b_r < n ? a.js + b_r : n;
     a.k = (int)(je - a.js);
     a.has_left = jt > 0;
-    unsigned gd = (unsigned)((c.ms + DIAG_WARPS - 1) / DIAG_WARPS);
-    k_diag<<<gd, DIAG_WARPS * 32, diag_smem, stream>>>(c, a);
-    g_launches++;
+    if (mc > 0) {
+      a.q0 = 0;
+      a.count = mc;
+      const int per = DWC * DG;
+      k_diag_cplx<<<(unsigned)((mc + per - 1) / per), DWC * 32, dsm_c, stream>>>(c, a);
+      g_launches++;
+    }
+    if (mr > 0) {
+      a.q0 = mc;
+      a.count = mr;
+      const int per = DWR * DG;
+      k_diag_real<<<(unsigned)((mr + per - 1) / per), DWR * 32, dsm_r, stream>>>(c, a);
+      g_launches++;
+    }
     if (g_timing) cudaEventRecord(ev[2 + 2 * jt], stream);
     if (jt > 0) {
       PanelArgs p;
@@ -1067,13 +514,24 @@ int64_t hsrq_tile_diag(int32_t k, int32_t b, const double* hdiag, const double* 
   a.t_status = status;
   a.t_b = b;
   a.t_hleft = hleft;
-  const size_t diag_smem = sizeof(DiagSmem);
-  if (!ck(cudaFuncSetAttribute(k_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem),
+  a.q0 = 0;
+  a.count = b;
+  const size_t dsm_r = sizeof(double) * (MAXK + DWR * (2 * MAXK * DG + 2 * MAXK));
+  const size_t dsm_c = sizeof(double) * (MAXK + DWC * (4 * MAXK * DG + 2 * MAXK));
+  if (!ck(cudaFuncSetAttribute(k_diag_real, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_r),
+          "attr") ||
+      !ck(cudaFuncSetAttribute(k_diag_cplx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_c),
           "attr"))
     return HSRQ_ERR_CUDA;
   if (!ck(cudaMemsetAsync(status, 0, sizeof(int64_t) * b, (cudaStream_t)stream), "memset"))
     return HSRQ_ERR_CUDA;
-  k_diag<<<(b + DIAG_WARPS - 1) / DIAG_WARPS, DIAG_WARPS * 32, diag_smem, (cudaStream_t)stream>>>(c, a);
+  if (lam_im) {
+    const int per = DWC * DG;
+    k_diag_cplx<<<(b + per - 1) / per, DWC * 32, dsm_c, (cudaStream_t)stream>>>(c, a);
+  } else {
+    const int per = DWR * DG;
+    k_diag_real<<<(b + per - 1) / per, DWR * 32, dsm_r, (cudaStream_t)stream>>>(c, a);
+  }
   if (!ck(cudaGetLastError(), "launch") || !ck(cudaStreamSynchronize((cudaStream_t)stream), "sync"))
     return HSRQ_ERR_CUDA;
   return 0;

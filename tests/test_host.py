@@ -1,0 +1,80 @@
+"""Host-side logic of the B200 path that needs no GPU: configuration errors,
+flop model, failure-report ordering, shard balancing."""
+
+import numpy as np
+import pytest
+
+from paper_2101_05063_b200 import (ConfigError, InviterConfig, SingularSystemError,
+                                   StructuralViolationError, chsrq3in, dhsrq3in, flops, hsrq3in)
+from paper_2101_05063_b200.parallel import local_selection, shard_bounds
+from paper_2101_05063_b200.solver import raise_first_failure
+
+
+def test_flop_model_matches_reference_counts():
+    # values of hessrq flops.py summed over one solve
+    assert flops.per_shift_flops(16000, 128, False) == 653287619
+    assert flops.per_shift_flops(16000, 128, True) == 1332957980
+    assert flops.per_shift_flops(256, 32, False) == 195254
+    assert flops.per_shift_flops(4000, 64, False) == 41683198
+    assert abs(flops.reference_flops(16000, 128, 3790, 6105) - 1.0614e13) < 1e10
+
+
+def test_config_errors_raise_before_any_device_work():
+    h = np.triu(np.ones((6, 6)), -1)
+    with pytest.raises(ConfigError):
+        dhsrq3in(h, [])
+    with pytest.raises(ConfigError):
+        chsrq3in(h, [1.0 + 0j])
+    hr = h.copy()
+    hr[3, 2] = 0.0
+    with pytest.raises(ConfigError):
+        dhsrq3in(hr, [0.5])
+    with pytest.raises(ConfigError):
+        hsrq3in(h, [0.5, 1 + 1j], InviterConfig(w_max=10))
+    with pytest.raises(ConfigError):
+        dhsrq3in(h, [0.5], InviterConfig(b_r=7))
+    with pytest.raises(ConfigError):
+        dhsrq3in(np.ones((5, 5)), [0.5])  # not Hessenberg
+
+
+def _code(phase, tile, row):
+    return (phase << 56) | (tile << 24) | row
+
+
+def test_first_failure_follows_reference_order():
+    codes = np.zeros(10, dtype=np.int64)
+    codes[7] = _code(2, 5, 3)   # singular, batch 1 (b_c=4)
+    codes[2] = _code(2, 1, 0)   # singular, batch 0, earlier batch wins
+    with pytest.raises(SingularSystemError) as e:
+        raise_first_failure(codes, 4, [(0, 10)])
+    assert e.value.shift_index == 2 and e.value.local_index == 0
+    # within a batch: higher tile column first (the sweep runs right to left)
+    codes[:] = 0
+    codes[1] = _code(2, 3, 9)
+    codes[0] = _code(2, 7, 2)
+    with pytest.raises(SingularSystemError) as e:
+        raise_first_failure(codes, 4, [(0, 10)])
+    assert e.value.shift_index == 0
+    # any degenerate rotation (reduction phase) precedes every singular pivot
+    codes[9] = _code(1, 0, 0)
+    with pytest.raises(StructuralViolationError):
+        raise_first_failure(codes, 4, [(0, 10)])
+    # a failure in the first call (real group) beats one in the second (complex)
+    codes[:] = 0
+    codes[8] = _code(2, 9, 9)
+    codes[1] = _code(2, 0, 0)
+    with pytest.raises(SingularSystemError) as e:
+        raise_first_failure(codes, 32, [(0, 5), (5, 10)])
+    assert e.value.shift_index == 1
+    raise_first_failure(np.zeros(4, dtype=np.int64), 4, [(0, 4)])  # no failure: no raise
+
+
+def test_shards_balance_flop_cost():
+    cuts = shard_bounds(3790, 6105, 8)
+    cost = np.concatenate([np.ones(3790), np.full(6105, 2.04)])
+    per = [cost[cuts[r]:cuts[r + 1]].sum() for r in range(8)]
+    assert cuts[0] == 0 and cuts[-1] == 9895
+    assert max(per) - min(per) <= 2.04 + 1e-9
+    eigs = np.concatenate([np.arange(5) + 0.5, np.arange(4) + 1j])
+    seen = np.concatenate([local_selection(eigs, r, 3)[0] for r in range(3)])
+    assert sorted(seen.tolist()) == list(range(9))
