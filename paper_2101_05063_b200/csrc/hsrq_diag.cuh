@@ -17,10 +17,8 @@
 // guards are evaluated from cheap monotone bounds first and exactly only
 // when a bound cannot prove protect_update == 1.
 
-constexpr int DP = 4;        // lanes per shift
-constexpr int DG = 32 / DP;  // shifts per warp
-constexpr int DWR = 4;       // warps per CTA, real kernel   (64 KB smem)
-constexpr int DWC = 2;       // warps per CTA, complex kernel (64 KB smem)
+// Lanes per shift (DP) and warps per CTA are template parameters; the host
+// picks the variant (see diag_launch in hsrq_kernels.cu).
 constexpr double DSLACK = 1.0 + 0x1p-46;
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -75,11 +73,14 @@ __device__ __forceinline__ void fill_col(const Ctx& c, const DiagArgs& a, double
   cp_commit();
 }
 
+template <int DP>
 __device__ __forceinline__ double gmax(double v) {  // max over the DP lanes of a group
-  double w = __shfl_xor_sync(FULL, v, 1);
-  v = w > v ? w : v;
-  w = __shfl_xor_sync(FULL, v, 2);
-  return w > v ? w : v;
+#pragma unroll
+  for (int o = 1; o < DP; o <<= 1) {
+    const double w = __shfl_xor_sync(FULL, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
 }
 
 __device__ __forceinline__ void record_fail(const Ctx& c, const DiagArgs& a, int64_t q, int phase,
@@ -128,7 +129,9 @@ __device__ __forceinline__ void put_rot(const Ctx& c, const DiagArgs& a, int64_t
 // ---------------------------------------------------------------------------
 // real shifts
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(DWR * 32) k_diag_real(Ctx c, DiagArgs a) {
+template <int DP, int DW>
+__global__ void __launch_bounds__(DW * 32) k_diag_real(Ctx c, DiagArgs a) {
+  constexpr int DG = 32 / DP;
   extern __shared__ __align__(16) double dsm[];
   double* hmax = dsm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(DWR * 32) k_diag_real(Ctx c, DiagArgs a) {
   double* hb = Xs + MAXK * DG;  // [2][MAXK] column buffers
   const int k = a.k;
   load_hmax(c, a, hmax);
-  const int64_t q = a.q0 + ((int64_t)blockIdx.x * DWR + warp) * DG + grp;
+  const int64_t q = a.q0 + ((int64_t)blockIdx.x * DW + warp) * DG + grp;
   bool live = q < a.q0 + a.count;
   if (live && !a.tile_mode && c.fail[q] != 0) live = false;
   const int64_t col = a.tile_mode ? 0 : 2 * c.mc + (q - c.mc);
@@ -191,8 +194,8 @@ __global__ void __launch_bounds__(DWR * 32) k_diag_real(Ctx c, DiagArgs a) {
       if (pl == 0) record_fail(c, a, q, HSRQ_KIND_SINGULAR, kp);
       live = false;
     }
-    xm = gmax(xm);
-    vm = gmax(vm);
+    xm = gmax<DP>(xm);
+    vm = gmax<DP>(vm);
     if (robust && live) {
       const double aphi = fabs(phi), ax = fabs(xk);
       if (aphi < 1.0 && ax > aphi * omega) {  // guard 1 (:144-151)
@@ -318,7 +321,7 @@ __global__ void __launch_bounds__(DWR * 32) k_diag_real(Ctx c, DiagArgs a) {
     const double z = fabs(VV(i));
     if (z > zm) zm = z;
   }
-  zm = gmax(zm);
+  zm = gmax<DP>(zm);
   if (live) {
     for (int j = k + pl; j < KP; j += DP) {
       bw[j] = 0.0;
@@ -345,7 +348,9 @@ __global__ void __launch_bounds__(DWR * 32) k_diag_real(Ctx c, DiagArgs a) {
 // ---------------------------------------------------------------------------
 // complex shifts (Im > 0), interleaved re/im columns 2q, 2q+1
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(DWC * 32) k_diag_cplx(Ctx c, DiagArgs a) {
+template <int DP, int DW>
+__global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
+  constexpr int DG = 32 / DP;
   extern __shared__ __align__(16) double dsm[];
   double* hmax = dsm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -357,7 +362,7 @@ __global__ void __launch_bounds__(DWC * 32) k_diag_cplx(Ctx c, DiagArgs a) {
   double* hb = Xi + MAXK * DG;  // [2][MAXK] column buffers
   const int k = a.k;
   load_hmax(c, a, hmax);
-  const int64_t q = a.q0 + ((int64_t)blockIdx.x * DWC + warp) * DG + grp;
+  const int64_t q = a.q0 + ((int64_t)blockIdx.x * DW + warp) * DG + grp;
   bool live = q < a.q0 + a.count;
   if (live && !a.tile_mode && c.fail[q] != 0) live = false;
   const int64_t col = a.tile_mode ? 0 : 2 * q;
@@ -419,8 +424,8 @@ __global__ void __launch_bounds__(DWC * 32) k_diag_cplx(Ctx c, DiagArgs a) {
       if (pl == 0) record_fail(c, a, q, HSRQ_KIND_SINGULAR, kp);
       live = false;
     }
-    xb = gmax(xb);
-    vb = gmax(vb);
+    xb = gmax<DP>(xb);
+    vb = gmax<DP>(vb);
     if (robust && live) {  // guard 1 (robust_trsv_complex :501-508)
       const double adlo = fmax(fabs(d.re), fabs(d.im));
       if (adlo < 1.0 && (fabs(xk.re) + fabs(xk.im)) * DSLACK > adlo * omega) {
@@ -457,8 +462,8 @@ __global__ void __launch_bounds__(DWC * 32) k_diag_cplx(Ctx c, DiagArgs a) {
         if (q1 > rm) rm = q1;
         if (q2 > bm) bm = q2;
       }
-      rm = gmax(rm);
-      bm = gmax(bm);
+      rm = gmax<DP>(rm);
+      bm = gmax<DP>(bm);
       if (exact2) {
         const int e = protect_update_e(bm, rm, cabs_(xk), omega);
         if (e < 0) {
@@ -608,7 +613,7 @@ __global__ void __launch_bounds__(DWC * 32) k_diag_cplx(Ctx c, DiagArgs a) {
     const double z = cabs_(mk(Vr[IX(i)], Vi[IX(i)]));
     if (z > zm) zm = z;
   }
-  zm = gmax(zm);
+  zm = gmax<DP>(zm);
   if (live) {
     for (int j = k + pl; j < KP; j += DP) {
       bw_re[j] = bw_im[j] = 0.0;

@@ -31,6 +31,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/hsrq.h"
@@ -212,6 +213,54 @@ bool ck(cudaError_t e, const char* what) {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Diagonal-kernel variants: DP lanes per shift, DW warps per CTA.
+int g_diag_dp = 8;  // HSRQ_DIAG_DP overrides (4, 8 or 16)
+
+template <int DP, int DW, bool CPLX>
+size_t diag_smem() {
+  return sizeof(double) * (MAXK + DW * ((CPLX ? 4 : 2) * MAXK * (32 / DP) + 2 * MAXK));
+}
+
+template <int DP, int DWR_, int DWC_>
+bool diag_attrs_v() {
+  return ck(cudaFuncSetAttribute(k_diag_real<DP, DWR_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)diag_smem<DP, DWR_, false>()), "attr diag r") &&
+         ck(cudaFuncSetAttribute(k_diag_cplx<DP, DWC_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)diag_smem<DP, DWC_, true>()), "attr diag c");
+}
+
+bool diag_attrs() {
+  static bool done = false;
+  if (done) return true;
+  const char* e = getenv("HSRQ_DIAG_DP");
+  if (e) g_diag_dp = atoi(e);
+  done = diag_attrs_v<4, 4, 2>() && diag_attrs_v<8, 6, 4>() && diag_attrs_v<16, 8, 8>();
+  return done;
+}
+
+template <int DP, int DWR_, int DWC_>
+void diag_launch_v(bool cplx, const Ctx& c, const DiagArgs& a, cudaStream_t s) {
+  const int64_t cnt = a.count;
+  if (cplx) {
+    const int per = DWC_ * (32 / DP);
+    k_diag_cplx<DP, DWC_><<<(unsigned)((cnt + per - 1) / per), DWC_ * 32,
+                            diag_smem<DP, DWC_, true>(), s>>>(c, a);
+  } else {
+    const int per = DWR_ * (32 / DP);
+    k_diag_real<DP, DWR_><<<(unsigned)((cnt + per - 1) / per), DWR_ * 32,
+                            diag_smem<DP, DWR_, false>(), s>>>(c, a);
+  }
+}
+
+void diag_launch(bool cplx, const Ctx& c, const DiagArgs& a, cudaStream_t s) {
+  if (g_diag_dp == 4)
+    diag_launch_v<4, 4, 2>(cplx, c, a, s);
+  else if (g_diag_dp == 16)
+    diag_launch_v<16, 8, 8>(cplx, c, a, s);
+  else
+    diag_launch_v<8, 6, 4>(cplx, c, a, s);
+}
+
 struct WsLayout {
   size_t cr, bop, ss, hm0, rs, hmk, xb, rsc, nfail, total;
 };
@@ -300,14 +349,9 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   }
 
   static bool attr_done = false;
-  const size_t dsm_r = sizeof(double) * (MAXK + DWR * (2 * MAXK * DG + 2 * MAXK));
-  const size_t dsm_c = sizeof(double) * (MAXK + DWC * (4 * MAXK * DG + 2 * MAXK));
   const size_t panel_smem = sizeof(PanelSmem);
   if (!attr_done) {
-    if (!ck(cudaFuncSetAttribute(k_diag_real, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_r),
-            "attr diag") ||
-        !ck(cudaFuncSetAttribute(k_diag_cplx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_c),
-            "attr diagc") ||
+    if (!diag_attrs() ||
         !ck(cudaFuncSetAttribute(k_panel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)panel_smem), "attr panel") ||
         !ck(cudaFuncSetAttribute(k_panel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -359,15 +403,13 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     if (mc > 0) {
       a.q0 = 0;
       a.count = mc;
-      const int per = DWC * DG;
-      k_diag_cplx<<<(unsigned)((mc + per - 1) / per), DWC * 32, dsm_c, stream>>>(c, a);
+      diag_launch(true, c, a, stream);
       g_launches++;
     }
     if (mr > 0) {
       a.q0 = mc;
       a.count = mr;
-      const int per = DWR * DG;
-      k_diag_real<<<(unsigned)((mr + per - 1) / per), DWR * 32, dsm_r, stream>>>(c, a);
+      diag_launch(false, c, a, stream);
       g_launches++;
     }
     if (g_timing) cudaEventRecord(ev[2 + 2 * jt], stream);
@@ -516,22 +558,10 @@ int64_t hsrq_tile_diag(int32_t k, int32_t b, const double* hdiag, const double* 
   a.t_hleft = hleft;
   a.q0 = 0;
   a.count = b;
-  const size_t dsm_r = sizeof(double) * (MAXK + DWR * (2 * MAXK * DG + 2 * MAXK));
-  const size_t dsm_c = sizeof(double) * (MAXK + DWC * (4 * MAXK * DG + 2 * MAXK));
-  if (!ck(cudaFuncSetAttribute(k_diag_real, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_r),
-          "attr") ||
-      !ck(cudaFuncSetAttribute(k_diag_cplx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm_c),
-          "attr"))
-    return HSRQ_ERR_CUDA;
+  if (!diag_attrs()) return HSRQ_ERR_CUDA;
   if (!ck(cudaMemsetAsync(status, 0, sizeof(int64_t) * b, (cudaStream_t)stream), "memset"))
     return HSRQ_ERR_CUDA;
-  if (lam_im) {
-    const int per = DWC * DG;
-    k_diag_cplx<<<(b + per - 1) / per, DWC * 32, dsm_c, (cudaStream_t)stream>>>(c, a);
-  } else {
-    const int per = DWR * DG;
-    k_diag_real<<<(b + per - 1) / per, DWR * 32, dsm_r, (cudaStream_t)stream>>>(c, a);
-  }
+  diag_launch(lam_im != nullptr, c, a, (cudaStream_t)stream);
   if (!ck(cudaGetLastError(), "launch") || !ck(cudaStreamSynchronize((cudaStream_t)stream), "sync"))
     return HSRQ_ERR_CUDA;
   return 0;
