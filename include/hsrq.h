@@ -113,6 +113,9 @@ int64_t hsrq_solve_group_async(const double* H, int64_t ldh, int64_t n, int32_t 
                                size_t ws_bytes, void* stream);
 int64_t hsrq_failure_count(void* ws, void* stream);
 
+/* Guard-path event counters (diagnostics): out_host[16]; reset != 0 zeroes them. */
+int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset);
+
 /* Kernel launches issued by the last solve on this thread (for accounting). */
 int64_t hsrq_last_launch_count(void);
 

@@ -43,6 +43,7 @@ SIGNATURES = {
     ),
     "hsrq_protect_update_batch": (_i64, [_p, _p, _p, _f64, _i64, _p, _p]),
     "hsrq_hypot_batch": (_i64, [_p, _p, _i64, _p, _p]),
+    "hsrq_debug_counters": (_i64, [_p, _i32]),
 }
 
 _lib = None

@@ -54,6 +54,10 @@ constexpr int SMAX = 8;      // max tile rows per CTA
 constexpr int PANEL_THREADS = 256;
 constexpr int KP = 128;      // stride of the B operand (K padded)
 
+// Event counters (guard paths taken), read with hsrq_debug_counters().
+__device__ unsigned long long g_ctr[16];
+#define HSRQ_COUNT(i) atomicAdd(&g_ctr[(i)], 1ULL)
+
 struct StepScalars {         // per shift, written by k_diag, read by k_panel
   double rho_re, rho_im;     // s0 * xbelow[0]      (update_rupdate :213)
   double zk_re, zk_im;       // Z[k-1]              (:302)
@@ -523,6 +527,17 @@ int64_t hsrq_solve_group(const double* H, int64_t ldh, int64_t n, int32_t b_r,
 }
 
 int64_t hsrq_last_launch_count(void) { return g_launches; }
+
+int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset) {
+  unsigned long long v[16];
+  if (cudaMemcpyFromSymbol(v, g_ctr, sizeof(v)) != cudaSuccess) return HSRQ_ERR_CUDA;
+  for (int i = 0; i < 16; i++) out_host[i] = (int64_t)v[i];
+  if (reset) {
+    unsigned long long z[16] = {0};
+    if (cudaMemcpyToSymbol(g_ctr, z, sizeof(z)) != cudaSuccess) return HSRQ_ERR_CUDA;
+  }
+  return 0;
+}
 void hsrq_set_timing(int32_t enable) { g_timing = enable; }
 void hsrq_phase_times(double* out_host) {
   for (int i = 0; i < 4; i++) out_host[i] = g_phase_ms[i];

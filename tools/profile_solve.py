@@ -30,3 +30,10 @@ for _ in range(a.reps):
     nf = gs.launch(start, True)
 torch.cuda.synchronize()
 print("failed", nf)
+import ctypes
+from paper_2101_05063_b200 import _lib
+cnt = np.zeros(16, dtype=np.int64)
+_lib.load().hsrq_debug_counters(ctypes.c_void_p(cnt.ctypes.data), 1)
+names = ["r_g1_fire", "r_g2_fire", "c_g1_exact", "c_g1_fire", "c_g2_exact", "c_g2_fire", "r_steps",
+         "c_steps", "scal_items", "scal_exact1", "scal_exact2", "panel_s3_exact_cta"]
+print({nm: int(v) for nm, v in zip(names, cnt)})
