@@ -252,14 +252,14 @@ def run_gpu(args):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    phase = np.zeros(4)
+    phase = np.zeros(5)
     launches = 0
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             step(timing=True)
             launches += int(lib.hsrq_last_launch_count())
-            pt = np.zeros(4)
+            pt = np.zeros(5)
             lib.hsrq_phase_times(ctypes.c_void_p(pt.ctypes.data))
             phase += pt
             gather()
@@ -380,8 +380,8 @@ def run_gpu(args):
         "tflops_frac_of_fp64_peak": ref_fl / (ms / 1e3) / 1e12 / (peak * world),
         "executed_tflops": exe_fl / (ms / 1e3) / 1e12,
         "eigenvectors_incl_conjugates_per_s": (m_total_r + 2 * m_total_c) / (ms / 1e3),
-        "phase_ms": {"diag": phase[0], "panel": phase[1], "backtransform": phase[2],
-                     "setup": phase[3]},
+        "phase_ms": {"diag": phase[0], "scalars": phase[4], "panel": phase[1],
+                     "backtransform": phase[2], "setup": phase[3]},
         "roofline": {
             "bound": "tensor", "kernel": "k_panel (DMMA f64)",
             "achieved": ach, "peak": peak, "unit": "TFLOP/s",

@@ -120,8 +120,8 @@ int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset);
 int64_t hsrq_last_launch_count(void);
 
 /* Per-phase device times (ms) of the last solve run with timing enabled:
- * out_host[0] = diagonal kernels, [1] = panel GEMM kernels, [2] = backtransform,
- * [3] = setup.  Enable with hsrq_set_timing(1) (adds events, serialises). */
+ * out_host[0] = diagonal kernels, [1] = panel GEMM kernels (k_panel), [2] =
+ * backtransform, [3] = setup, [4] = guard-scalar kernels (k_scalars).  Enable with hsrq_set_timing(1) (adds events, serialises). */
 void hsrq_set_timing(int32_t enable);
 void hsrq_phase_times(double* out_host);
 

@@ -205,7 +205,7 @@ __global__ void k_hypot_batch(const double* x, const double* y, int64_t count, d
 thread_local char g_err[512] = "";
 thread_local int64_t g_launches = 0;
 int g_timing = 0;
-double g_phase_ms[4] = {0, 0, 0, 0};
+double g_phase_ms[5] = {0, 0, 0, 0, 0};
 
 bool ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
@@ -368,7 +368,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     attr_done = true;
   }
   // Optional per-launch timing: events around every launch, one sync at the end.
-  const int nev = 2 * c.N + 4;
+  const int nev = 3 * c.N + 4;
   cudaEvent_t* ev = nullptr;
   if (g_timing) {
     ev = new cudaEvent_t[nev];
@@ -416,7 +416,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
       diag_launch(false, c, a, stream);
       g_launches++;
     }
-    if (g_timing) cudaEventRecord(ev[2 + 2 * jt], stream);
+    if (g_timing) cudaEventRecord(ev[2 + 3 * jt], stream);
     if (jt > 0) {
       PanelArgs p;
       p.jt = jt;
@@ -427,6 +427,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
       const int64_t nsc = (int64_t)jt * c.ms;
       k_scalars<<<(unsigned)((nsc + 127) / 128), 128, 0, stream>>>(c, p, rsc);
       g_launches++;
+      if (g_timing) cudaEventRecord(ev[3 + 3 * jt], stream);
       dim3 gp((unsigned)(c.ncol_pad / BN), (unsigned)((jt + S - 1) / S));
       const bool seg16 = (b_r % 16) == 0;
       if (a16 && seg16)
@@ -439,7 +440,10 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
         k_panel<false, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
       g_launches++;
     }
-    if (g_timing) cudaEventRecord(ev[3 + 2 * jt], stream);
+    if (g_timing) {
+      if (jt == 0) cudaEventRecord(ev[3 + 3 * jt], stream);
+      cudaEventRecord(ev[4 + 3 * jt], stream);
+    }
   }
   k_backtransform<<<(unsigned)((c.ms + BT_WARPS - 1) / BT_WARPS), BT_WARPS * 32, 0, stream>>>(
       c, alpha_exp, norms, log2norm);
@@ -448,16 +452,19 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     cudaEventRecord(ev[nev - 2], stream);
     cudaEventSynchronize(ev[nev - 2]);
     float t;
-    double t_diag = 0, t_panel = 0;
-    // launch order: ev[1] | diag(N-1) ev[2+2(N-1)] panel ev[3+2(N-1)] | diag(N-2) ...
+    double t_diag = 0, t_panel = 0, t_scal = 0;
+    // per column: ev[prev] diag ev[2+3jt] scalars ev[3+3jt] panel ev[4+3jt]
     int prev = 1;
     for (int jt = c.N - 1; jt >= 0; --jt) {
-      cudaEventElapsedTime(&t, ev[prev], ev[2 + 2 * jt]);
+      cudaEventElapsedTime(&t, ev[prev], ev[2 + 3 * jt]);
       t_diag += t;
-      cudaEventElapsedTime(&t, ev[2 + 2 * jt], ev[3 + 2 * jt]);
+      cudaEventElapsedTime(&t, ev[2 + 3 * jt], ev[3 + 3 * jt]);
+      t_scal += t;
+      cudaEventElapsedTime(&t, ev[3 + 3 * jt], ev[4 + 3 * jt]);
       t_panel += t;
-      prev = 3 + 2 * jt;
+      prev = 4 + 3 * jt;
     }
+    g_phase_ms[4] = t_scal;
     cudaEventElapsedTime(&t, ev[prev], ev[nev - 2]);
     g_phase_ms[2] = t;
     cudaEventElapsedTime(&t, ev[0], ev[1]);
@@ -540,7 +547,7 @@ int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset) {
 }
 void hsrq_set_timing(int32_t enable) { g_timing = enable; }
 void hsrq_phase_times(double* out_host) {
-  for (int i = 0; i < 4; i++) out_host[i] = g_phase_ms[i];
+  for (int i = 0; i < 5; i++) out_host[i] = g_phase_ms[i];
 }
 
 int64_t hsrq_tile_diag(int32_t k, int32_t b, const double* hdiag, const double* hleft,

@@ -351,7 +351,23 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
   const double lr0 = v0 ? c.lam_re[q0] : 0.0, li0 = (v0 && cplx) ? c.lam_im[q0] : 0.0;
   const double lr1 = v1 ? c.lam_re[q1] : 0.0;
   // pass 1: X'' = x2 X' - (fx x2) (A Zs); bounds of max|X''|, max|Cr_old|
-  double xa[EP_RPT], xb[EP_RPT], ca[EP_RPT], cb[EP_RPT];
+  double xa[EP_RPT], xb[EP_RPT], ca[EP_RPT], cb[EP_RPT], hh[EP_RPT];
+  // issue every global load of this thread's rows first (one latency), then compute
+  {
+    const double* __restrict__ X0 = c.X + gc0 * c.ldx + row0;
+    const double* __restrict__ C0 = c.Cr + gc0 * c.ldx + row0;
+    const double* __restrict__ H0 = c.H + (p.js - 1) * c.ldh + row0;
+#pragma unroll
+    for (int j = 0; j < EP_RPT; j++) {
+      const int r = rp + EP_ROWS * j;
+      const bool ok = r < rows_valid;
+      xa[j] = (ok && v0) ? X0[r] : 0.0;
+      xb[j] = (ok && v1) ? X0[c.ldx + r] : 0.0;
+      ca[j] = (ok && v0) ? C0[r] : 0.0;
+      cb[j] = (ok && v1) ? C0[c.ldx + r] : 0.0;
+      hh[j] = ok ? H0[r] : 0.0;
+    }
+  }
   {
     double mb0 = 0.0, mb1 = 0.0, mr0 = 0.0, mr1 = 0.0;
     int seg = SEG16 ? 0 : -1;
@@ -360,32 +376,27 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
       const int r = rp + EP_ROWS * j;
       const bool ok = r < rows_valid;
       const int sg = r / c.b_r;
-      double x0 = 0.0, x1 = 0.0, c0v = 0.0, c1v = 0.0;
+      double x0 = 0.0, x1 = 0.0;
+      const double c0v = ca[j], c1v = cb[j];
       if (ok) {
-        const int64_t grow = row0 + r;
-        const double h0 = c.H[(p.js - 1) * c.ldh + grow];
+        const double h0 = hh[j];
         const bool last = ((r + 1) % c.b_r == 0) && (tile0 + sg == jt - 1);
         if (v0) {
           const RowScalars& s0 = sm.rsc[sg][cl0];
-          x0 = step1_apply(c.X[gc0 * c.ldx + grow], s0.fb, s0.rr, s0.ri, h0, last, cplx, false, lr0,
-                           li0);
+          x0 = step1_apply(xa[j], s0.fb, s0.rr, s0.ri, h0, last, cplx, false, lr0, li0);
           if (s0.x2 < 1.0) x0 *= s0.x2;
           x0 -= (s0.fx * s0.x2) * sm.u.C[2 * cl0 + 1][r];
-          c0v = c.Cr[gc0 * c.ldx + grow];
         }
         if (v1) {
           const RowScalars& s1 = sm.rsc[sg][cl0 + 1];
-          x1 = step1_apply(c.X[(gc0 + 1) * c.ldx + grow], s1.fb, s1.rr, s1.ri, h0, last, cplx,
-                           true, cplx ? lr0 : lr1, li0);
+          x1 = step1_apply(xb[j], s1.fb, s1.rr, s1.ri, h0, last, cplx, true, cplx ? lr0 : lr1,
+                           li0);
           if (s1.x2 < 1.0) x1 *= s1.x2;
           x1 -= (s1.fx * s1.x2) * sm.u.C[2 * cl0 + 3][r];
-          c1v = c.Cr[(gc0 + 1) * c.ldx + grow];
         }
       }
       xa[j] = x0;
       xb[j] = x1;
-      ca[j] = c0v;
-      cb[j] = c1v;
       double qb0, qb1, qr0, qr1;
       if (cplx) {
         qb0 = qb1 = fabs(x0) + fabs(x1);
