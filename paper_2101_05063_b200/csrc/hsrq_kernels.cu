@@ -89,6 +89,7 @@ struct Ctx {
   unsigned long long* nfail;
   int robust, mode;
   double omega;
+  int diag_gemm_only;  // diagnostics: panel without epilogue (HSRQ_PANEL_GEMM_ONLY=1)
 };
 
 __device__ __forceinline__ void col_of_shift(const Ctx& c, int64_t q, bool& cplx, int64_t& col) {
@@ -344,6 +345,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   c.nfail = (unsigned long long*)(w + L.nfail);
   c.robust = robust;
   c.mode = mode;
+  c.diag_gemm_only = getenv("HSRQ_PANEL_GEMM_ONLY") ? atoi(getenv("HSRQ_PANEL_GEMM_ONLY")) : 0;
   c.omega = robust ? (1.7976931348623157e308 / 2.0) / (double)b_r
                    : HUGE_VAL;
   // the crossover block shares X's leading dimension
