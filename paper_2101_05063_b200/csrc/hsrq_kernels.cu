@@ -90,6 +90,8 @@ struct Ctx {
   int robust, mode;
   double omega;
   int diag_gemm_only;  // diagnostics: panel without epilogue (HSRQ_PANEL_GEMM_ONLY=1)
+  unsigned long long* diag_tl;  // HSRQ_TIMELINE: per-CTA phase timestamps
+  int diag_tl_jt;
 };
 
 __device__ __forceinline__ void col_of_shift(const Ctx& c, int64_t q, bool& cplx, int64_t& col) {
@@ -206,6 +208,7 @@ __global__ void k_hypot_batch(const double* x, const double* y, int64_t count, d
 thread_local char g_err[512] = "";
 thread_local int64_t g_launches = 0;
 int g_timing = 0;
+unsigned long long* g_tl = nullptr;
 double g_phase_ms[5] = {0, 0, 0, 0, 0};
 
 bool ck(cudaError_t e, const char* what) {
@@ -217,6 +220,8 @@ bool ck(cudaError_t e, const char* what) {
 }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+int g_panel_fast = 1;  // HSRQ_PANEL_FAST=0 forces the general epilogue (testing)
 
 // Diagonal-kernel variants: DP lanes per shift, DW warps per CTA.
 int g_diag_dp = 8;  // HSRQ_DIAG_DP overrides (4, 8 or 16)
@@ -237,6 +242,8 @@ bool diag_attrs_v() {
 bool diag_attrs() {
   static bool done = false;
   if (done) return true;
+  const char* pf = getenv("HSRQ_PANEL_FAST");
+  if (pf) g_panel_fast = atoi(pf);
   const char* e = getenv("HSRQ_DIAG_DP");
   if (e) g_diag_dp = atoi(e);
   done = diag_attrs_v<4, 4, 2>() && diag_attrs_v<8, 6, 4>() && diag_attrs_v<16, 8, 8>();
@@ -346,6 +353,16 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   c.robust = robust;
   c.mode = mode;
   c.diag_gemm_only = getenv("HSRQ_PANEL_GEMM_ONLY") ? atoi(getenv("HSRQ_PANEL_GEMM_ONLY")) : 0;
+  c.diag_tl = nullptr;
+  c.diag_tl_jt = -1;
+  if (getenv("HSRQ_TIMELINE")) {
+    static unsigned long long* tl = nullptr;
+    if (!tl) cudaMalloc(&tl, 8192 * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(tl, 0, 8192 * 8 * sizeof(unsigned long long), stream);
+    c.diag_tl = tl;
+    c.diag_tl_jt = atoi(getenv("HSRQ_TIMELINE"));
+    g_tl = tl;
+  }
   c.omega = robust ? (1.7976931348623157e308 / 2.0) / (double)b_r
                    : HUGE_VAL;
   // the crossover block shares X's leading dimension
@@ -358,14 +375,16 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   const size_t panel_smem = sizeof(PanelSmem);
   if (!attr_done) {
     if (!diag_attrs() ||
-        !ck(cudaFuncSetAttribute(k_panel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        !ck(cudaFuncSetAttribute(k_panel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)panel_smem), "attr panel") ||
-        !ck(cudaFuncSetAttribute(k_panel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        !ck(cudaFuncSetAttribute(k_panel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)panel_smem), "attr panel") ||
-        !ck(cudaFuncSetAttribute(k_panel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        !ck(cudaFuncSetAttribute(k_panel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)panel_smem), "attr panel") ||
-        !ck(cudaFuncSetAttribute(k_panel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)panel_smem), "attr panel"))
+        !ck(cudaFuncSetAttribute(k_panel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)panel_smem), "attr panel") ||
+        !ck(cudaFuncSetAttribute(k_panel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)panel_smem), "attr panel fast"))
       return HSRQ_ERR_CUDA;
     attr_done = true;
   }
@@ -432,14 +451,16 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
       if (g_timing) cudaEventRecord(ev[3 + 3 * jt], stream);
       dim3 gp((unsigned)(c.ncol_pad / BN), (unsigned)((jt + S - 1) / S));
       const bool seg16 = (b_r % 16) == 0;
-      if (a16 && seg16)
-        k_panel<true, true><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
+      if (a16 && b_r == BM && g_panel_fast)
+        k_panel<true, true, true><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
+      else if (a16 && seg16)
+        k_panel<true, true, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
       else if (a16)
-        k_panel<true, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
+        k_panel<true, false, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
       else if (seg16)
-        k_panel<false, true><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
+        k_panel<false, true, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
       else
-        k_panel<false, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
+        k_panel<false, false, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
       g_launches++;
     }
     if (g_timing) {
@@ -536,6 +557,15 @@ int64_t hsrq_solve_group(const double* H, int64_t ldh, int64_t n, int32_t b_r,
 }
 
 int64_t hsrq_last_launch_count(void) { return g_launches; }
+
+int64_t hsrq_debug_timeline(unsigned long long* out_host) {
+  if (!g_tl) return -1;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(out_host, g_tl, 8192 * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+                 cudaSuccess
+             ? 0
+             : HSRQ_ERR_CUDA;
+}
 
 int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset) {
   unsigned long long v[16];
