@@ -345,6 +345,17 @@ def run_gpu(args):
         return 0
 
     peak, peak_src, hbm = load_peaks()
+    traffic, traffic_note = None, None
+    prof = os.path.join(ROOT, "profiles", "ncu_r01_k_panel_cfg5_jt84.json")
+    if os.path.exists(prof) and n == 16000:
+        with open(prof) as f:
+            pj = json.load(f)
+        rd = float(pj["dram__bytes_read.sum"].split()[0]) * 1e9
+        wr = float(pj["dram__bytes_write.sum"].split()[0]) * 1e9
+        traffic = rd + wr
+        traffic_note = {"launch": pj["launch"], "algorithmic_bytes": pj["algorithmic_bytes"],
+                        "ratio": traffic / pj["algorithmic_bytes"],
+                        "source": "profiles/ncu_r01_k_panel_cfg5_jt84.json (ncu --set full)"}
     nvec = m_total_r + m_total_c
     ref_fl = F.reference_flops(n, b_r, m_total_r, m_total_c)
     exe_fl = F.executed_flops(n, b_r, m_total_r, m_total_c)
@@ -385,7 +396,7 @@ def run_gpu(args):
         "roofline": {
             "bound": "tensor", "kernel": "k_panel (DMMA f64)",
             "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-            "frac": (ach / peak) if ach else None, "traffic": None,
+            "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_detail": traffic_note,
             "peak_source": peak_src,
             "executed_achieved": my_exe / (panel_ms / 1e3) / 1e12 if panel_ms > 0 else None,
             "algorithmic": "reference flop model (hessrq flops.py) ReduceOffdiag+Update flops of "
