@@ -85,3 +85,21 @@ def test_restart_stream():
         v = _next_start(1e-14, 37, prev, 0x5EED, att)
         prev.append(v.copy())
         assert np.array_equal(v, want)
+
+
+def test_singular_shift_reported_like_reference(oracle):
+    """Exactly singular shifted systems: same shift_index / local_index as
+    the reference's SingularSystemError (backsolve.py:53-59)."""
+    g = golden("singular")
+    ncase = 0
+    for t in g["tags"]:
+        h, lam = g[f"{t}_h"], g[f"{t}_lam"]
+        n = h.shape[0]
+        b = np.ones((n, lam.size)) + (0j if int(g[f"{t}_cplx"]) else 0)
+        for b_r, b_c, shift, row in g[f"{t}_hits"]:
+            with pytest.raises(oracle.OracleError) as e:
+                oracle.solve(h, lam, b, int(b_r), int(b_c), robust=True, mode="solve")
+            assert e.value.phase == 2
+            assert (e.value.shift_index, e.value.local_index) == (shift, row)
+            ncase += 1
+    assert ncase >= 4

@@ -212,7 +212,80 @@ def gen_inviter():
     save("inviter", **store)
 
 
+def _reference_error(f):
+    """The SingularSystemError a reference call raises (unwrapping TaskError), or None."""
+    from hessrq.core import SingularSystemError
+
+    try:
+        f()
+    except Exception as e:  # noqa: BLE001 - scheduler wraps the kernel error in TaskError
+        c = e
+        while c is not None and not isinstance(c, SingularSystemError):
+            c = c.__cause__
+        if c is None:
+            raise
+        return c
+    return None
+
+
+def gen_singular():
+    """Exactly singular shifted systems (SingularSystemError parity).
+
+    Small-integer Hessenberg matrices with an integer (real case) or Gaussian
+    integer (complex case) eigenvalue: the shifted matrix is exactly singular
+    and the reference's final pivot is exactly 0.0.  Recorded per case: the
+    shift_index / local_index the reference reports (backsolve.py:53-59),
+    for the solver and for the inverse-iteration driver.
+    """
+    store = {}
+    tags = []
+    rng = np.random.default_rng(3)
+    n = 8
+    want_real, want_cplx = 4, 2
+    for trial in range(20000):
+        if want_real == 0 and want_cplx == 0:
+            break
+        h = np.triu(rng.integers(-2, 3, (n, n))).astype(float)
+        h[np.arange(1, n), np.arange(n - 1)] = rng.choice([-2.0, -1.0, 1.0, 2.0], n - 1)
+        ev = np.linalg.eigvals(h)
+        for lam in ev:
+            lr, li = round(lam.real), round(lam.imag)
+            if abs(lam - complex(lr, li)) > 1e-9:
+                continue
+            cplx = li != 0
+            if (cplx and (want_cplx == 0 or li < 0)) or (not cplx and want_real == 0):
+                continue
+            z = complex(lr, li)
+            lam_v = (np.array([z + 0.25, z, z + 0.5j if cplx else z + 0.5, z]) if cplx
+                     else np.array([lr + 0.25, lr, lr + 0.5, lr], dtype=float))
+            b = np.ones((n, 4)) + (0j if cplx else 0)
+            f = chsrq3 if cplx else dhsrq3
+            hit = []
+            for b_r, b_c in ((8, 4), (3, 2), (2, 1)):
+                e = _reference_error(lambda: f(h, lam_v, b, b_r=b_r, b_c=b_c))
+                if e is not None:
+                    hit.append((b_r, b_c, e.shift_index, e.local_index))
+            if not hit:
+                continue
+            ei = _reference_error(lambda: hsrq3in(h, np.array([z]), InviterConfig(b_r=3, b_c=2)))
+            t = f"g{len(tags)}"
+            store[f"{t}_h"] = np.asfortranarray(h)
+            store[f"{t}_lam"] = lam_v
+            store[f"{t}_cplx"] = np.array(int(cplx))
+            store[f"{t}_hits"] = np.array(hit, dtype=np.int64)
+            store[f"{t}_inviter"] = np.array(
+                [-1, -1] if ei is None else [ei.shift_index, ei.local_index], dtype=np.int64)
+            tags.append(t)
+            if cplx:
+                want_cplx -= 1
+            else:
+                want_real -= 1
+            break
+    save("singular", tags=np.array(tags), **store)
+
+
 if __name__ == "__main__":
+    gen_singular()
     gen_scalars()
     gen_tiles()
     gen_solves()
