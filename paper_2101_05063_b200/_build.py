@@ -17,7 +17,13 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhsrq_b200.so")
 SOURCES = [os.path.join(CSRC, "hsrq_kernels.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "hsrq_device.cuh"), os.path.join(ROOT, "include", "hsrq.h")]
+DEPS = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh")))
+DEPS.append(os.path.join(ROOT, "include", "hsrq.h"))
+
+def variant_lib(name):
+    """Diagnostics builds (e.g. "counters": guard-path event counters compiled
+    in, read with hsrq_debug_counters), loaded with HSRQ_LIB_VARIANT=name."""
+    return os.path.join(HERE, f"libhsrq_b200_{name}.so")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -40,15 +46,18 @@ def stale():
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force=False, verbose=False):
-    if not force and not stale():
+def build(force=False, verbose=False, variant=None, defines=()):
+    out = variant_lib(variant) if variant else LIB
+    if not force and not variant and not stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *SOURCES]
+    extra = [f"-D{d}" for d in defines]
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp",
+           *SOURCES]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-from ._build import LIB, build, stale
+from ._build import LIB, build, stale, variant_lib
 
 _c = ctypes
 _p = ctypes.c_void_p
@@ -54,11 +54,14 @@ def load(auto_build=True):
     global _lib
     if _lib is not None:
         return _lib
-    if auto_build and stale():
+    path = LIB
+    if os.environ.get("HSRQ_LIB_VARIANT"):  # diagnostics build (tools/profile_solve.py)
+        path = variant_lib(os.environ["HSRQ_LIB_VARIANT"])
+    elif auto_build and stale():
         build()
-    if not os.path.exists(LIB):
-        raise ImportError(f"libhsrq_b200.so not built ({LIB}); run __graft_entry__.build()")
-    lib = ctypes.CDLL(LIB)
+    if not os.path.exists(path):
+        raise ImportError(f"{os.path.basename(path)} not built ({path}); run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
         f = getattr(lib, name)
         f.restype = res

@@ -92,6 +92,14 @@ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
   return cplx{(areal * ratio + aimag) / denom, (aimag * ratio - areal) / denom};
 }
 
+// floor(log2(x)) for positive normal x; -2000 for 0 / subnormal, 2000 for inf/NaN.
+__device__ __forceinline__ int ilogb_pos(double x) {
+  const int b = (int)((__double_as_longlong(x) >> 52) & 0x7ff);
+  if (b == 0) return -2000;
+  if (b == 0x7ff) return 2000;
+  return b - 1023;
+}
+
 // pow2floor (numba_backend.py:37-44) as an exponent.
 __device__ __forceinline__ int pow2floor_e(double x) {
   if (x <= 0.0 || x != x) return -1074;

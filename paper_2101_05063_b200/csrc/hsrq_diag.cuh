@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_real(Ctx c, DiagArgs a) {
     if (robust && live) {
       const double aphi = fabs(phi), ax = fabs(xk);
       if (aphi < 1.0 && ax > aphi * omega) {  // guard 1 (:144-151)
+        if (pl == 0) HSRQ_COUNT(0);
         const int e = pow2floor_e(aphi * omega / ax);
         const double xi = p2(e);
         for (int i = pl; i < k; i += DP) XX(i) *= xi;
@@ -210,7 +211,9 @@ __global__ void __launch_bounds__(DW * 32) k_diag_real(Ctx c, DiagArgs a) {
     xk = xk / phi;
     if (robust && live) {  // guard 2 (:153-168)
       const int e = protect_update_e(xm, vm + hmax[kp] + fabs(lam), fabs(xk), omega);
+      if (pl == 0) HSRQ_COUNT(6);
       if (e < 0) {
+        if (pl == 0) HSRQ_COUNT(1);
         const double xi = p2(e);
         for (int i = pl; i < k; i += DP) XX(i) *= xi;
         xk *= xi;
@@ -430,7 +433,9 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
       const double adlo = fmax(fabs(d.re), fabs(d.im));
       if (adlo < 1.0 && (fabs(xk.re) + fabs(xk.im)) * DSLACK > adlo * omega) {
         const double ad = cabs_(d), ax = cabs_(xk);
+        if (pl == 0) HSRQ_COUNT(2);
         if (ad < 1.0 && ax > ad * omega) {
+          if (pl == 0) HSRQ_COUNT(3);
           const int e = pow2floor_e(ad * omega / ax);
           const cplx xi = mk(p2(e), 0.0);
           for (int i = pl; i < k; i += DP) {
@@ -447,35 +452,86 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
     xk = cdiv(xk, d);
     // guard 2 (:510-523): protect_update(max|x_i|, max|r_i|, |x_kp|), i < kp
     bool exact2 = false;
+    double rb = 0.0;
     if (robust && live) {
-      const double rb = ((fabs(cr) + fabs(ci)) * vb + fabs(sv) * (hmax[kp] + fabs(lre) + fabs(lim))) *
-                        DSLACK;
+      rb = ((fabs(cr) + fabs(ci)) * vb + fabs(sv) * (hmax[kp] + fabs(lre) + fabs(lim))) * DSLACK;
       exact2 = !protect_update_is_one(xb * DSLACK, rb, (fabs(xk.re) + fabs(xk.im)) * DSLACK, omega);
+      if (pl == 0) HSRQ_COUNT(7);
+      if (pl == 0 && exact2) HSRQ_COUNT(4);
     }
-    if (__any_sync(FULL, exact2)) {  // rare: exact hypot maxima over the R column and x
-      double rm = 0.0, bm = 0.0;
+#ifdef HSRQ_EXP_NOEXACT2
+    exact2 = false;  // timing experiment only: results are wrong
+#endif
+    if (__any_sync(FULL, exact2)) {
+      // The bounds could not prove xi = 1.  Certify protect_update's exponent
+      // from an interval around the two maxima instead of evaluating glibc
+      // moduli row by row: scaled squared moduli (one pass, no hypot) give
+      // max|.| to within 2^-47; protect_update_e is monotone in both norms
+      // (hsrq_device.cuh), so equal exponents at both interval ends are the
+      // exact exponent.  Otherwise (a binade edge, or bounds too loose to
+      // scale by) fall back to the exact maxima.
+      if (lane == 0) HSRQ_COUNT(12);
+      const int ex = ilogb_pos(xb), er = ilogb_pos(rb);
+      const double sx = p2(-max(-1000, min(1020, ex))), sr = p2(-max(-1000, min(1020, er)));
+      double tx = 0.0, tr = 0.0;
       for (int i = pl; i < kp; i += DP) {
         cplx t = mk(hcol[i], 0.0);
         if (i == kp - 1) t = csub(t, mk(lre, lim));
         const cplx ri = csub(cmul(ccj, mk(Vr[IX(i)], Vi[IX(i)])), cmul(svc, t));
-        const double q1 = cabs_(ri), q2 = cabs_(mk(Xr[IX(i)], Xi[IX(i)]));
-        if (q1 > rm) rm = q1;
-        if (q2 > bm) bm = q2;
+        const double a1 = ri.re * sr, b1 = ri.im * sr;
+        const double a2 = Xr[IX(i)] * sx, b2 = Xi[IX(i)] * sx;
+        const double t1 = a1 * a1 + b1 * b1, t2 = a2 * a2 + b2 * b2;
+        if (t1 > tr) tr = t1;
+        if (t2 > tx) tx = t2;
       }
-      rm = gmax<DP>(rm);
-      bm = gmax<DP>(bm);
+      tr = gmax<DP>(tr);
+      tx = gmax<DP>(tx);
+      bool full = false;
+      int e = 0;
       if (exact2) {
-        const int e = protect_update_e(bm, rm, cabs_(xk), omega);
-        if (e < 0) {
-          const cplx xi = mk(p2(e), 0.0);
-          for (int i = pl; i < k; i += DP) {
-            const cplx t = cmul(mk(Xr[IX(i)], Xi[IX(i)]), xi);
-            Xr[IX(i)] = t.re;
-            Xi[IX(i)] = t.im;
-          }
-          xk = cmul(xk, xi);
-          gexp += e;
+        const double ax = cabs_(xk);
+        if (ex > -1000 && ex < 1020 && er > -1000 && er < 1020 && tx >= 0x1p-960 &&
+            tr >= 0x1p-960 && tx <= 16.0 && tr <= 16.0) {
+          const double qx = sqrt(tx), qr = sqrt(tr);
+          const double bl = (qx - qx * 0x1p-47) * p2(ex), bh = (qx + qx * 0x1p-47) * p2(ex);
+          const double rl = (qr - qr * 0x1p-47) * p2(er), rh = (qr + qr * 0x1p-47) * p2(er);
+          e = protect_update_e(bl, rl, ax, omega);
+          full = e != protect_update_e(bh, rh, ax, omega);
+          if (full && pl == 0) HSRQ_COUNT(14);
+        } else {
+          full = true;
+          if (pl == 0) HSRQ_COUNT(15);
+#ifdef HSRQ_COUNTERS
+          if (pl == 0 && lane == 0 && blockIdx.x == 0 && kp == 100)
+            printf("jt %d ex %d er %d tx %g tr %g xb %g rb %g\n", a.jt, ex, er, tx, tr, xb, rb);
+#endif
         }
+      }
+      if (__any_sync(FULL, full)) {  // exact glibc moduli (rare)
+        if (lane == 0) HSRQ_COUNT(13);
+        double rm = 0.0, bm = 0.0;
+        for (int i = pl; i < kp; i += DP) {
+          cplx t = mk(hcol[i], 0.0);
+          if (i == kp - 1) t = csub(t, mk(lre, lim));
+          const cplx ri = csub(cmul(ccj, mk(Vr[IX(i)], Vi[IX(i)])), cmul(svc, t));
+          const double q1 = cabs_(ri), q2 = cabs_(mk(Xr[IX(i)], Xi[IX(i)]));
+          if (q1 > rm) rm = q1;
+          if (q2 > bm) bm = q2;
+        }
+        rm = gmax<DP>(rm);
+        bm = gmax<DP>(bm);
+        if (full) e = protect_update_e(bm, rm, cabs_(xk), omega);
+      }
+      if (exact2 && e < 0) {
+        if (pl == 0) HSRQ_COUNT(5);
+        const cplx xi = mk(p2(e), 0.0);
+        for (int i = pl; i < k; i += DP) {
+          const cplx t = cmul(mk(Xr[IX(i)], Xi[IX(i)]), xi);
+          Xr[IX(i)] = t.re;
+          Xi[IX(i)] = t.im;
+        }
+        xk = cmul(xk, xi);
+        gexp += e;
       }
     }
     if (pl == (kp % DP)) {

@@ -56,7 +56,11 @@ constexpr int KP = 128;      // stride of the B operand (K padded)
 
 // Event counters (guard paths taken), read with hsrq_debug_counters().
 __device__ unsigned long long g_ctr[16];
+#ifdef HSRQ_COUNTERS
 #define HSRQ_COUNT(i) atomicAdd(&g_ctr[(i)], 1ULL)
+#else
+#define HSRQ_COUNT(i) ((void)0)
+#endif
 
 struct StepScalars {         // per shift, written by k_diag, read by k_panel
   double rho_re, rho_im;     // s0 * xbelow[0]      (update_rupdate :213)
@@ -223,30 +227,46 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 int g_panel_fast = 1;  // HSRQ_PANEL_FAST=0 forces the general epilogue (testing)
 
-// Diagonal-kernel variants: DP lanes per shift, DW warps per CTA.
-int g_diag_dp = 8;  // HSRQ_DIAG_DP overrides (4, 8 or 16)
+// Diagonal-kernel variants: DP lanes per shift, DWR / DWC warps per CTA for
+// the real / complex kernel.  HSRQ_DIAG="DP,DWR,DWC" selects one of the
+// instantiated variants (tuning); the default is the measured best.
+struct DiagVariant {
+  int dp, dwr, dwc;
+};
+DiagVariant g_diag = {4, 4, 2};
 
 template <int DP, int DW, bool CPLX>
 size_t diag_smem() {
   return sizeof(double) * (MAXK + DW * ((CPLX ? 4 : 2) * MAXK * (32 / DP) + 2 * MAXK));
 }
 
-template <int DP, int DWR_, int DWC_>
-bool diag_attrs_v() {
-  return ck(cudaFuncSetAttribute(k_diag_real<DP, DWR_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)diag_smem<DP, DWR_, false>()), "attr diag r") &&
-         ck(cudaFuncSetAttribute(k_diag_cplx<DP, DWC_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)diag_smem<DP, DWC_, true>()), "attr diag c");
-}
+#define HSRQ_DIAG_VARIANTS(X) X(4, 4, 2) X(8, 6, 4) X(16, 8, 8) X(2, 2, 1) X(4, 2, 1) X(4, 4, 4) X(4, 8, 4)
 
 bool diag_attrs() {
   static bool done = false;
   if (done) return true;
   const char* pf = getenv("HSRQ_PANEL_FAST");
   if (pf) g_panel_fast = atoi(pf);
-  const char* e = getenv("HSRQ_DIAG_DP");
-  if (e) g_diag_dp = atoi(e);
-  done = diag_attrs_v<4, 4, 2>() && diag_attrs_v<8, 6, 4>() && diag_attrs_v<16, 8, 8>();
+  const char* e = getenv("HSRQ_DIAG");
+  if (e) {
+    DiagVariant v;
+    if (sscanf(e, "%d,%d,%d", &v.dp, &v.dwr, &v.dwc) == 3) g_diag = v;
+  }
+  bool known = false;
+#define HSRQ_KNOWN(DP, DWR, DWC) known |= g_diag.dp == DP && g_diag.dwr == DWR && g_diag.dwc == DWC;
+  HSRQ_DIAG_VARIANTS(HSRQ_KNOWN)
+#undef HSRQ_KNOWN
+  if (!known) g_diag = DiagVariant{4, 4, 2};
+  bool ok = true;
+#define HSRQ_ATTR(DP, DWR, DWC)                                                                  \
+  if (g_diag.dp == DP && g_diag.dwr == DWR && g_diag.dwc == DWC)                                 \
+    ok = ck(cudaFuncSetAttribute(k_diag_real<DP, DWR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)diag_smem<DP, DWR, false>()), "attr diag r") &&              \
+         ck(cudaFuncSetAttribute(k_diag_cplx<DP, DWC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)diag_smem<DP, DWC, true>()), "attr diag c");
+  HSRQ_DIAG_VARIANTS(HSRQ_ATTR)
+#undef HSRQ_ATTR
+  done = ok;
   return done;
 }
 
@@ -265,12 +285,14 @@ void diag_launch_v(bool cplx, const Ctx& c, const DiagArgs& a, cudaStream_t s) {
 }
 
 void diag_launch(bool cplx, const Ctx& c, const DiagArgs& a, cudaStream_t s) {
-  if (g_diag_dp == 4)
-    diag_launch_v<4, 4, 2>(cplx, c, a, s);
-  else if (g_diag_dp == 16)
-    diag_launch_v<16, 8, 8>(cplx, c, a, s);
-  else
-    diag_launch_v<8, 6, 4>(cplx, c, a, s);
+#define HSRQ_LAUNCH(DP, DWR, DWC)                                       \
+  if (g_diag.dp == DP && g_diag.dwr == DWR && g_diag.dwc == DWC) {      \
+    diag_launch_v<DP, DWR, DWC>(cplx, c, a, s);                         \
+    return;                                                             \
+  }
+  HSRQ_DIAG_VARIANTS(HSRQ_LAUNCH)
+#undef HSRQ_LAUNCH
+  diag_launch_v<4, 4, 2>(cplx, c, a, s);
 }
 
 struct WsLayout {
@@ -417,6 +439,23 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   if (g_timing) cudaEventRecord(ev[1], stream);
   const bool a16 = (ldh % 2 == 0) && (b_r % 2 == 0);
   const int S = std::min(SMAX, std::max(1, BM / b_r));
+  // side stream + fork/join events for the concurrent real diagonal kernel
+  // (one set per host thread; the side stream is created with the caller's
+  // device current and never synchronises with the legacy default stream)
+  thread_local cudaStream_t side = nullptr;
+  thread_local int side_dev = -1;
+  thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (side_dev != dev) {
+      if (!ck(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "side stream") ||
+          !ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "fork event") ||
+          !ck(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "join event"))
+        return HSRQ_ERR_CUDA;
+      side_dev = dev;
+    }
+  }
   for (int jt = c.N - 1; jt >= 0; --jt) {
     DiagArgs a;
     memset(&a, 0, sizeof(a));
@@ -425,17 +464,29 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     int64_t je = a.js + b_r < n ? a.js + b_r : n;
     a.k = (int)(je - a.js);
     a.has_left = jt > 0;
+    // Real and complex shifts are independent columns: their diagonal
+    // kernels run concurrently (the real one on a side stream, forked and
+    // joined with events), so the latency-bound sweeps share the SMs.
+    const bool fork = mc > 0 && mr > 0 && side != nullptr;
+    if (fork) {
+      cudaEventRecord(ev_fork, stream);
+      cudaStreamWaitEvent(side, ev_fork, 0);
+    }
+    if (mr > 0) {
+      a.q0 = mc;
+      a.count = mr;
+      diag_launch(false, c, a, fork ? side : stream);
+      g_launches++;
+    }
     if (mc > 0) {
       a.q0 = 0;
       a.count = mc;
       diag_launch(true, c, a, stream);
       g_launches++;
     }
-    if (mr > 0) {
-      a.q0 = mc;
-      a.count = mr;
-      diag_launch(false, c, a, stream);
-      g_launches++;
+    if (fork) {
+      cudaEventRecord(ev_join, side);
+      cudaStreamWaitEvent(stream, ev_join, 0);
     }
     if (g_timing) cudaEventRecord(ev[2 + 3 * jt], stream);
     if (jt > 0) {

@@ -83,6 +83,7 @@ __global__ void k_scalars(Ctx c, PanelArgs p, RowScalars* RSc) {
     return;
   }
   const double omega = c.omega;
+  HSRQ_COUNT(8);
   const bool shifted = it == jt - 1;
   const double lr = c.lam_re[q], li = cplx ? c.lam_im[q] : 0.0;
   const int64_t r0 = (int64_t)it * c.b_r;
@@ -97,6 +98,7 @@ __global__ void k_scalars(Ctx c, PanelArgs p, RowScalars* RSc) {
   if (cplx) {
     bmax *= BOUND_SLACK;
     if (!protect_update_is_one(p2(g - be) * bmax, hm0 + alam, arho, omega)) {
+      HSRQ_COUNT(9);
       double m = 0.0;  // exact max |b| (rare: near overflow)
       for (int r = 0; r < c.b_r; r++) {
         double v = ghypot(c.X[col * c.ldx + r0 + r], c.X[(col + 1) * c.ldx + r0 + r]);
@@ -130,6 +132,7 @@ __global__ void k_scalars(Ctx c, PanelArgs p, RowScalars* RSc) {
     const double alb = shifted ? fabs(lr) + fabs(li) : 0.0;
     const double b1 = (o.fb * bmax + arb * hm0 + alb * arb) * BOUND_SLACK;
     if (!protect_update_is_one(b1, rs, zmax, omega)) {
+      HSRQ_COUNT(10);
       double m = 0.0;  // exact max |X'| (rare)
       for (int r = 0; r < c.b_r; r++) {
         const double h0 = c.H[(p.js - 1) * c.ldh + r0 + r];
@@ -393,6 +396,7 @@ __device__ __forceinline__ void epilogue_b128(const Ctx& c, const PanelArgs& p, 
     }
   }
   if (__syncthreads_or(my_need)) {  // rare: exact glibc moduli for flagged complex columns
+    if (tid == 0) HSRQ_COUNT(11);
     double hb = 0.0, hr = 0.0;
     if (cplx && v0) {
 #pragma unroll
@@ -764,6 +768,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
     sm.dex[sg][cc] = dx;
   }
   if (__syncthreads_or(my_need)) {  // rare: exact hypot maxima for flagged complex columns
+    if (tid == 0) HSRQ_COUNT(11);
     for (int e = tid; e < 2 * SMAX * BN; e += PANEL_THREADS) (&sm.red[0][0][0])[e] = 0ULL;
     __syncthreads();
     if (cplx && v0) {

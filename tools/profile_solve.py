@@ -1,4 +1,9 @@
-"""One inverse-iteration solve attempt of a BASELINE config on cuda:0 (for ncu)."""
+"""One inverse-iteration solve attempt of a BASELINE config on cuda:0 (for ncu).
+
+With HSRQ_LIB_VARIANT=counters it loads the diagnostics build
+(libhsrq_b200_counters.so, ``_build.build(variant="counters",
+defines=["HSRQ_COUNTERS"])``) and prints how often each guard path ran.
+"""
 import argparse
 import os
 import sys
@@ -26,14 +31,21 @@ dev = torch.device("cuda", 0)
 gs = GroupSolver(DeviceHessenberg(hm, dev), b_r, ec.size, er.size)
 gs.set_shifts(ec, er)
 start = torch.full((hm.n,), np.finfo(float).eps * hm.infinity_norm(), dtype=torch.float64, device=dev)
+import ctypes
+from paper_2101_05063_b200 import _lib
+L = _lib.load()
+nf = gs.launch(start, True)  # warm-up
+L.hsrq_set_timing(1)
 for _ in range(a.reps):
     nf = gs.launch(start, True)
 torch.cuda.synchronize()
-print("failed", nf)
-import ctypes
-from paper_2101_05063_b200 import _lib
+pt = np.zeros(5)
+L.hsrq_phase_times(ctypes.c_void_p(pt.ctypes.data))
+L.hsrq_set_timing(0)
+print("failed", nf, "phase ms (diag, panel, backtransform, setup, scalars):", np.round(pt, 2).tolist())
 cnt = np.zeros(16, dtype=np.int64)
 _lib.load().hsrq_debug_counters(ctypes.c_void_p(cnt.ctypes.data), 1)
 names = ["r_g1_fire", "r_g2_fire", "c_g1_exact", "c_g1_fire", "c_g2_exact", "c_g2_fire", "r_steps",
-         "c_steps", "scal_items", "scal_exact1", "scal_exact2", "panel_s3_exact_cta"]
+         "c_steps", "scal_items", "scal_exact1", "scal_exact2", "panel_s3_exact_cta",
+         "c_g2_exact_warpsteps", "c_g2_full_warpsteps", "c_g2_mismatch", "c_g2_invalid"]
 print({nm: int(v) for nm, v in zip(names, cnt)})
