@@ -40,6 +40,14 @@ struct RowScalars {
 
 constexpr double BOUND_SLACK = 1.0 + 0x1p-46;  // covers the roundings inside a bound
 
+// Epilogue mapping (k_panel, k_scalars): thread -> column pair pc (CTA
+// columns 2pc, 2pc+1; a complex shift or two real shifts) and rows rp + 16 j.
+// For b_r % 16 == 0 (SEG16) the 16 threads of a pair share a segment for each
+// j, so segment maxima reduce with shuffles; otherwise through shared-memory
+// atomics.
+constexpr int EP_ROWS = 16;                       // threads per column pair
+constexpr int EP_RPT = BM / EP_ROWS;              // rows per thread (8)
+
 // X' = fb X + rho h0 (- lambda rho on the last row of the shifted tile):
 // update_rupdate :224-231 / cupdate_crupdate :621-633, one component.
 __device__ __forceinline__ double step1_apply(double x, double fb, double rr, double ri, double h0,
@@ -60,55 +68,42 @@ __device__ __forceinline__ double step1_apply(double x, double fb, double rr, do
   return x;
 }
 
-// One thread per (tile row it < jt, shift q).
-__global__ void k_scalars(Ctx c, PanelArgs p, RowScalars* RSc) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int jt = p.jt;
-  if (t >= (int64_t)jt * c.ms) return;
-  const int it = (int)(t / c.ms);
-  const int64_t q = t % c.ms;
+// ---- update steps 1-2 for one (tile row it < jt, shift q) ----
+// Step 1 (update_rupdate :211-231 / cupdate_crupdate :600-633).  bmax =
+// max|b| over the tile rows: exact for real columns; for complex columns
+// either the exact glibc-modulus maximum (bmax_exact) or an upper bound.
+// Returns false when a complex bound cannot prove the guard's result: the
+// caller then supplies the exact maximum and calls again.
+__device__ __forceinline__ bool scalars_step1(const Ctx& c, int jt, int it, int64_t q,
+                                              double bmax, bool bmax_exact, RowScalars& o) {
   const bool cplx = q < c.mc;
-  const int64_t col = cplx ? 2 * q : 2 * c.mc + (q - c.mc);
   const StepScalars st = c.SS[q];
-  RowScalars o;
   o.pad = 0;
+  o.x2 = 1.0;
   if (c.fail[q] != 0 || !c.robust) {
-    o.fb = o.fx = o.x2 = 1.0;
+    o.fb = o.fx = 1.0;
     o.rr = st.rho_re;
     o.ri = st.rho_im;
     o.zkr = st.zk_re;
     o.zki = st.zk_im;
     o.dexp = 0;
-    RSc[t] = o;
-    return;
+    return true;
   }
   const double omega = c.omega;
-  HSRQ_COUNT(8);
   const bool shifted = it == jt - 1;
   const double lr = c.lam_re[q], li = cplx ? c.lam_im[q] : 0.0;
-  const int64_t r0 = (int64_t)it * c.b_r;
   const int ae = c.E[(int64_t)jt * c.ms + q];
   const int be = c.E[(int64_t)it * c.ms + q];
   const int g = ae < be ? ae : be;
   const double alam = shifted ? (cplx ? ghypot(lr, li) : fabs(lr)) : 0.0;
   const double hm0 = c.HM0[(int64_t)jt * c.N + it];
   const double arho = cplx ? ghypot(st.rho_re, st.rho_im) : fabs(st.rho_re);
-  // ---- step 1 (:211-231) ----
-  double bmax = c.XB[(int64_t)it * c.ms + q];  // real: exact max|b|; complex: bound
-  if (cplx) {
+  if (cplx && !bmax_exact) {
     bmax *= BOUND_SLACK;
-    if (!protect_update_is_one(p2(g - be) * bmax, hm0 + alam, arho, omega)) {
-      HSRQ_COUNT(9);
-      double m = 0.0;  // exact max |b| (rare: near overflow)
-      for (int r = 0; r < c.b_r; r++) {
-        double v = ghypot(c.X[col * c.ldx + r0 + r], c.X[(col + 1) * c.ldx + r0 + r]);
-        if (v > m) m = v;
-      }
-      bmax = m;
-    }
+    if (!protect_update_is_one(p2(g - be) * bmax, hm0 + alam, arho, omega)) return false;
   }
   const int xe1 = protect_update_e(p2(g - be) * bmax, hm0 + alam, arho, omega);
-  int d = xe1 + g;
+  const int d = xe1 + g;
   o.fb = p2(d - be);
   o.fx = p2(d - ae);
   o.rr = st.rho_re;
@@ -123,43 +118,159 @@ __global__ void k_scalars(Ctx c, PanelArgs p, RowScalars* RSc) {
     o.zkr *= o.fx;
     o.zki *= o.fx;
   }
-  o.x2 = 1.0;
-  // ---- step 2 (:255-278): bound of max|X'| = fb bmax + |rho| hmax0 + |lambda rho| ----
-  if (p.k > 1) {
-    const double zmax = o.fx != 1.0 ? o.fx * st.zmax : st.zmax;
-    const double rs = c.RS[(int64_t)jt * c.N + it];
-    const double arb = cplx ? fabs(o.rr) + fabs(o.ri) : fabs(o.rr);
-    const double alb = shifted ? fabs(lr) + fabs(li) : 0.0;
-    const double b1 = (o.fb * bmax + arb * hm0 + alb * arb) * BOUND_SLACK;
-    if (!protect_update_is_one(b1, rs, zmax, omega)) {
+  o.dexp = d;
+  return true;
+}
+
+// Upper bound of max|X'| (X' = fb b + rho h0 - lambda rho e_last) from the
+// step-1 record and the bound/exact bmax: fb bmax + |rho| hmax0 + |lambda rho|.
+__device__ __forceinline__ double scalars_step2_bound(const Ctx& c, int jt, int it, int64_t q,
+                                                      double bmax, const RowScalars& o) {
+  const bool cplx = q < c.mc;
+  const bool shifted = it == jt - 1;
+  const double lr = c.lam_re[q], li = cplx ? c.lam_im[q] : 0.0;
+  const double hm0 = c.HM0[(int64_t)jt * c.N + it];
+  const double arb = cplx ? fabs(o.rr) + fabs(o.ri) : fabs(o.rr);
+  const double alb = shifted ? fabs(lr) + fabs(li) : 0.0;
+  return (o.fb * bmax + arb * hm0 + alb * arb) * BOUND_SLACK;
+}
+
+// Step 2 (:255-278) = protect_update(max|X'|, row-sum bound, max|Z|) on an
+// interval [xlo, xhi] around the exact max|X'| (xlo == xhi: the exact value).
+// protect_update_e is monotone, so equal exponents at both ends are the exact
+// exponent; returns false when the interval straddles an exponent change.
+__device__ __forceinline__ bool scalars_step2(const Ctx& c, int jt, int it, int64_t q, double xlo,
+                                              double xhi, RowScalars& o) {
+  const StepScalars st = c.SS[q];
+  const double zmax = o.fx != 1.0 ? o.fx * st.zmax : st.zmax;
+  const double rs = c.RS[(int64_t)jt * c.N + it];
+  const int e = protect_update_e(xlo, rs, zmax, c.omega);
+  if (xhi != xlo && e != protect_update_e(xhi, rs, zmax, c.omega)) return false;
+  if (e < 0) {
+    o.x2 = p2(e);
+    o.dexp += e;
+    o.zkr *= o.x2;
+    o.zki *= o.x2;
+  }
+  return true;
+}
+
+// "Step 2 leaves xi = 1" proved from an upper bound of max|X'|.
+__device__ __forceinline__ bool scalars_step2_is_one(const Ctx& c, int jt, int it, int64_t q,
+                                                     double xbound, const RowScalars& o) {
+  const StepScalars st = c.SS[q];
+  const double zmax = o.fx != 1.0 ? o.fx * st.zmax : st.zmax;
+  return protect_update_is_one(xbound, c.RS[(int64_t)jt * c.N + it], zmax, c.omega);
+}
+
+// Max over a tile-row segment of X' = fb b + rho h0 (- lambda rho on the
+// shifted tile's last row): real -> exact max|X'|; complex -> (bound
+// max(|re|+|im|), max of the squared moduli scaled by sc).  Rows are read
+// as 16-byte pairs when aligned (the thread streams its own segment).
+template <bool CPLX>
+__device__ __forceinline__ void seg_xprime_max(const double* __restrict__ Xr,
+                                               const double* __restrict__ Xi,
+                                               const double* __restrict__ H0, int nrow,
+                                               bool pairs, double fb, double rr, double ri,
+                                               bool shifted, double lr, double li, double sc,
+                                               double& bm, double& tm) {
+  bm = 0.0;
+  tm = 0.0;
+  auto row = [&](double xr0, double xi0, double h, int r) {
+    const bool last = shifted && r == nrow - 1;
+    if (CPLX) {
+      const double xr = step1_apply(xr0, fb, rr, ri, h, last, true, false, lr, li);
+      const double xi = step1_apply(xi0, fb, rr, ri, h, last, true, true, lr, li);
+      bm = fmax(bm, fabs(xr) + fabs(xi));
+      const double u = xr * sc, w = xi * sc;
+      tm = fmax(tm, u * u + w * w);
+    } else {
+      bm = fmax(bm, fabs(step1_apply(xr0, fb, rr, ri, h, last, false, false, lr, li)));
+    }
+  };
+  if (pairs) {
+    const double2* X2 = reinterpret_cast<const double2*>(Xr);
+    const double2* I2 = reinterpret_cast<const double2*>(Xi);
+    const double2* H2 = reinterpret_cast<const double2*>(H0);
+#pragma unroll 4
+    for (int r2 = 0; r2 < nrow / 2; r2++) {
+      const double2 x = X2[r2], h = H2[r2];
+      const double2 y = CPLX ? I2[r2] : make_double2(0.0, 0.0);
+      row(x.x, y.x, h.x, 2 * r2);
+      row(x.y, y.y, h.y, 2 * r2 + 1);
+    }
+  } else {
+    for (int r = 0; r < nrow; r++) row(Xr[r], CPLX ? Xi[r] : 0.0, H0[r], r);
+  }
+}
+
+// k_scalars: update steps 1-2, one thread per (tile row it < jt, shift q),
+// resolved before the panel GEMM.  Guards are evaluated from bounds (step 1
+// from XB, step 2 from fb bmax + |rho| hmax0 + |lambda rho|); only when a
+// bound fails does the thread read its b segment for the exact maximum --
+// for complex columns as scaled squared moduli certified on an interval (see
+// k_diag_cplx guard 2), glibc moduli only at a binade edge.
+__global__ void k_scalars(Ctx c, PanelArgs p, RowScalars* RSc) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int jt = p.jt;
+  if (t >= (int64_t)jt * c.ms) return;
+  const int it = (int)(t / c.ms);
+  const int64_t q = t % c.ms;
+  const bool cplx = q < c.mc;
+  const int64_t col = cplx ? 2 * q : 2 * c.mc + (q - c.mc);
+  const int64_t r0 = (int64_t)it * c.b_r;
+  const double* Xr = c.X + col * c.ldx + r0;
+  const double* Xi = Xr + c.ldx;
+  RowScalars o;
+  HSRQ_COUNT(8);
+  double bmax = c.XB[(int64_t)it * c.ms + q];  // real: exact max|b|; complex: bound
+  if (!scalars_step1(c, jt, it, q, bmax, !cplx, o)) {
+    HSRQ_COUNT(9);
+    double m = 0.0;  // exact max |b| (rare: near overflow)
+    for (int r = 0; r < c.b_r; r++) m = fmax(m, ghypot(Xr[r], Xi[r]));
+    bmax = m;
+    scalars_step1(c, jt, it, q, bmax, true, o);
+  } else if (cplx) {
+    bmax *= BOUND_SLACK;
+  }
+  if (p.k > 1 && c.robust && c.fail[q] == 0) {
+    const double b1 = scalars_step2_bound(c, jt, it, q, bmax, o);
+    if (!scalars_step2_is_one(c, jt, it, q, b1, o)) {
       HSRQ_COUNT(10);
-      double m = 0.0;  // exact max |X'| (rare)
-      for (int r = 0; r < c.b_r; r++) {
-        const double h0 = c.H[(p.js - 1) * c.ldh + r0 + r];
-        const bool last = shifted && r == c.b_r - 1;
-        if (cplx) {
-          double xr = step1_apply(c.X[col * c.ldx + r0 + r], o.fb, o.rr, o.ri, h0, last, true,
-                                  false, lr, li);
-          double xi = step1_apply(c.X[(col + 1) * c.ldx + r0 + r], o.fb, o.rr, o.ri, h0, last,
-                                  true, true, lr, li);
-          double v = ghypot(xr, xi);
-          if (v > m) m = v;
-        } else {
-          double v = fabs(step1_apply(c.X[col * c.ldx + r0 + r], o.fb, o.rr, o.ri, h0, last,
-                                      false, false, lr, li));
-          if (v > m) m = v;
+      const bool shifted = it == jt - 1;
+      const double lr = c.lam_re[q], li = cplx ? c.lam_im[q] : 0.0;
+      const double* H0 = c.H + (p.js - 1) * c.ldh + r0;
+      const bool pairs = ((c.ldx | c.ldh | c.b_r) & 1) == 0 && ((p.js - 1) * c.ldh) % 2 == 0;
+      double bm, tm;
+      if (!cplx) {
+        seg_xprime_max<false>(Xr, Xi, H0, c.b_r, pairs, o.fb, o.rr, o.ri, shifted, lr, li, 1.0,
+                              bm, tm);
+        scalars_step2(c, jt, it, q, bm, bm, o);
+      } else {
+        const int es = ilogb_pos(b1);
+        const double sc = p2(-max(-1000, min(1020, es)));
+        seg_xprime_max<true>(Xr, Xi, H0, c.b_r, pairs, o.fb, o.rr, o.ri, shifted, lr, li, sc, bm,
+                             tm);
+        bool done = scalars_step2_is_one(c, jt, it, q, bm * BOUND_SLACK, o);
+        if (!done && es > -1000 && es < 1020 && tm >= 0x1p-960 && tm <= 16.0) {
+          const double qt = sqrt(tm);
+          done = scalars_step2(c, jt, it, q, (qt - qt * 0x1p-47) * p2(es),
+                               (qt + qt * 0x1p-47) * p2(es), o);
         }
-      }
-      const int xe2 = protect_update_e(m, rs, zmax, omega);
-      if (xe2 < 0) {
-        o.x2 = p2(xe2);
-        d += xe2;
-        o.zkr *= o.x2;
-        o.zki *= o.x2;
+        if (!done) {  // binade edge: exact glibc moduli
+          HSRQ_COUNT(11);
+          double m = 0.0;
+          for (int r = 0; r < c.b_r; r++) {
+            const bool last = shifted && r == c.b_r - 1;
+            const double xr = step1_apply(Xr[r], o.fb, o.rr, o.ri, H0[r], last, true, false, lr, li);
+            const double xi = step1_apply(Xi[r], o.fb, o.rr, o.ri, H0[r], last, true, true, lr, li);
+            m = fmax(m, ghypot(xr, xi));
+          }
+          scalars_step2(c, jt, it, q, m, m, o);
+        }
       }
     }
   }
-  o.dexp = d;
   RSc[t] = o;
 }
 
@@ -225,12 +336,6 @@ __device__ __forceinline__ void panel_load(const Ctx& c, const PanelArgs& p, Pan
   }
 }
 
-// Epilogue mapping: thread -> column pair pc (CTA columns 2pc, 2pc+1; a
-// complex shift or two real shifts) and rows rp + 16 j.  For b_r % 16 == 0
-// (SEG16) the 16 threads of a pair share a segment for each j, so segment
-// maxima reduce with shuffles; otherwise through shared-memory atomics.
-constexpr int EP_ROWS = 16;                       // threads per column pair
-constexpr int EP_RPT = BM / EP_ROWS;              // rows per thread (8)
 
 template <bool SEG16>
 __device__ __forceinline__ void seg_max2(PanelSmem& sm, int slot, int sg, int cl0, double v0,
