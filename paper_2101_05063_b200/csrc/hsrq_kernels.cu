@@ -54,6 +54,9 @@ constexpr int SMAX = 8;      // max tile rows per CTA
 constexpr int PANEL_THREADS = 256;
 constexpr int KP = 128;      // stride of the B operand (K padded)
 
+// k_panel fast path: prefetch the epilogue tiles to L2 (HSRQ_PANEL_PREFETCH=0 disables)
+__device__ __constant__ int g_panel_prefetch = 1;
+
 // Event counters (guard paths taken), read with hsrq_debug_counters().
 __device__ unsigned long long g_ctr[16];
 #ifdef HSRQ_COUNTERS
@@ -247,6 +250,11 @@ bool diag_attrs() {
   if (done) return true;
   const char* pf = getenv("HSRQ_PANEL_FAST");
   if (pf) g_panel_fast = atoi(pf);
+  const char* pp = getenv("HSRQ_PANEL_PREFETCH");
+  if (pp) {
+    int v = atoi(pp);
+    cudaMemcpyToSymbol(g_panel_prefetch, &v, sizeof(int));
+  }
   const char* e = getenv("HSRQ_DIAG");
   if (e) {
     DiagVariant v;

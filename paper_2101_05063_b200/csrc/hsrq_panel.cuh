@@ -654,6 +654,18 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
     if (s < nk) panel_load<A16>(c, p, sm, s, s, row0, rows_valid, col0);
     cp_commit();
   }
+  if (FAST && g_panel_prefetch) {
+    // pull this CTA's epilogue operands (X and Cr tiles: 32 columns x 128
+    // rows, 8 lines of 128 B each) towards L2 while the main loop runs
+    for (int L = tid; L < 2 * BN * (BM / 16); L += PANEL_THREADS) {
+      const int arr = L / (BN * (BM / 16)), cc = (L / (BM / 16)) % BN, seg = L % (BM / 16);
+      const int64_t col = col0 + cc;
+      if (col < c.ncol) {
+        const double* a = (arr ? c.Cr : c.X) + col * c.ldx + row0 + seg * 16;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+      }
+    }
+  }
   // per (segment, column) records of steps 1-2 (k_scalars) and red init
   for (int e = tid; e < SMAX * BN; e += PANEL_THREADS) {
     const int sg = e / BN, cc = e % BN;
