@@ -508,7 +508,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
       k_scalars<<<(unsigned)((nsc + 127) / 128), 128, 0, stream>>>(c, p, rsc);
       g_launches++;
       if (g_timing) cudaEventRecord(ev[3 + 3 * jt], stream);
-      dim3 gp((unsigned)(c.ncol_pad / BN), (unsigned)((jt + S - 1) / S));
+      dim3 gp((unsigned)((jt + S - 1) / S), (unsigned)(c.ncol_pad / BN));
       const bool seg16 = (b_r % 16) == 0;
       if (a16 && b_r == BM && g_panel_fast)
         k_panel<true, true, true><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);

@@ -627,18 +627,20 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int S = p.S;
-  const int tile0 = blockIdx.y * S;
+  // grid: x = tile-row block (fastest), y = column block, so consecutive CTAs
+  // reuse one B-operand block (and the whole H panel stays L2-resident)
+  const int tile0 = blockIdx.x * S;
   const int ntiles = min(S, p.jt - tile0);
   const int64_t row0 = (int64_t)tile0 * c.b_r;
   const int rows_valid = ntiles * c.b_r;
-  const int64_t col0 = (int64_t)blockIdx.x * BN;
+  const int64_t col0 = (int64_t)blockIdx.y * BN;
   const int nk = (p.k + BK - 1) / BK;
   const int jt = p.jt;
   const double omega = c.omega;
   const bool robust = c.robust;
 
   // diagnostic timeline (HSRQ_TIMELINE=jt): per CTA smid + globaltimer at phase marks
-  const unsigned lin_ = blockIdx.y * gridDim.x + blockIdx.x;
+  const unsigned lin_ = blockIdx.x * gridDim.y + blockIdx.y;
   const bool tl_ = c.diag_tl != nullptr && jt == c.diag_tl_jt && lin_ < 8192 && tid == 0;
   unsigned long long* tlp_ = tl_ ? c.diag_tl + 8 * lin_ : nullptr;
   if (tl_) {
