@@ -223,22 +223,23 @@ __global__ void __launch_bounds__(DW * 32) k_diag_real(Ctx c, DiagArgs a) {
     if (pl == (kp % DP)) XX(kp) = xk;
     const double tau1 = ss * xk, tau2 = cc * xk;
     double nxm = 0.0, nvm = 0.0;
-#pragma unroll 2
-    for (int i = pl; i < kp; i += DP) {
+#pragma unroll 4
+    for (int i = pl; i < kp - 1; i += DP) {
       const double hi = hcol[i];
       double vv = VV(i), xx = XX(i);
-      if (i < kp - 1) {
-        xx = (xx - tau2 * vv) + tau1 * hi;
-        vv = cc * hi + ss * vv;
-        if (fabs(xx) > nxm) nxm = fabs(xx);
-        if (fabs(vv) > nvm) nvm = fabs(vv);
-      } else {
-        const double hd = hi - lam;
-        xx = (xx - tau2 * vv) + tau1 * hd;
-        vv = cc * hd + ss * vv;
-      }
+      xx = (xx - tau2 * vv) + tau1 * hi;
+      vv = cc * hi + ss * vv;
+      if (fabs(xx) > nxm) nxm = fabs(xx);
+      if (fabs(vv) > nvm) nvm = fabs(vv);
       VV(i) = vv;
       XX(i) = xx;
+    }
+    if (pl == (kp - 1) % DP) {  // the shifted row (diagonal entry h - lambda)
+      const int i = kp - 1;
+      const double hd = hcol[i] - lam;
+      const double vv = VV(i), xx = XX(i);
+      XX(i) = (xx - tau2 * vv) + tau1 * hd;
+      VV(i) = cc * hd + ss * vv;
     }
     xm = nxm;
     vm = nvm;
@@ -474,15 +475,15 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
       const int ex = ilogb_pos(xb), er = ilogb_pos(rb);
       const double sx = p2(-max(-1000, min(1020, ex))), sr = p2(-max(-1000, min(1020, er)));
       double tx = 0.0, tr = 0.0;
+#pragma unroll 2
       for (int i = pl; i < kp; i += DP) {
-        cplx t = mk(hcol[i], 0.0);
-        if (i == kp - 1) t = csub(t, mk(lre, lim));
+        const cplx t = i == kp - 1 ? csub(mk(hcol[i], 0.0), mk(lre, lim)) : mk(hcol[i], 0.0);
         const cplx ri = csub(cmul(ccj, mk(Vr[IX(i)], Vi[IX(i)])), cmul(svc, t));
         const double a1 = ri.re * sr, b1 = ri.im * sr;
         const double a2 = Xr[IX(i)] * sx, b2 = Xi[IX(i)] * sx;
         const double t1 = a1 * a1 + b1 * b1, t2 = a2 * a2 + b2 * b2;
-        if (t1 > tr) tr = t1;
-        if (t2 > tx) tx = t2;
+        tr = t1 > tr ? t1 : tr;
+        tx = t2 > tx ? t2 : tx;
       }
       tr = gmax<DP>(tr);
       tx = gmax<DP>(tx);
@@ -540,24 +541,30 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
     }
     double nxb = 0.0, nvb = 0.0;
 #pragma unroll 2
-    for (int i = pl; i < kp; i += DP) {
+    for (int i = pl; i < kp - 1; i += DP) {
       const double hi = hcol[i];
       const cplx v = mk(Vr[IX(i)], Vi[IX(i)]);
       cplx x = mk(Xr[IX(i)], Xi[IX(i)]);
-      cplx t = mk(hi, 0.0);
-      if (i == kp - 1) t = csub(t, mk(lre, lim));
-      const cplx ri = csub(cmul(ccj, v), cmul(svc, t));  // R[i, kp]
+      const cplx ri = csub(cmul(ccj, v), cmul(svc, mk(hi, 0.0)));  // R[i, kp]
       x = csub(x, cmul(xk, ri));
-      cplx vn;
-      if (i < kp - 1) {
-        vn = mk(cr * hi + sv * v.re, ci * hi + sv * v.im);
-        const double bx = fabs(x.re) + fabs(x.im), bv = fabs(vn.re) + fabs(vn.im);
-        if (bx > nxb) nxb = bx;
-        if (bv > nvb) nvb = bv;
-      } else {
-        const double tre = hi - lre, tim = -lim;
-        vn = mk((cr * tre - ci * tim) + sv * v.re, (cr * tim + ci * tre) + sv * v.im);
-      }
+      const cplx vn = mk(cr * hi + sv * v.re, ci * hi + sv * v.im);
+      const double bx = fabs(x.re) + fabs(x.im), bv = fabs(vn.re) + fabs(vn.im);
+      if (bx > nxb) nxb = bx;
+      if (bv > nvb) nvb = bv;
+      Vr[IX(i)] = vn.re;
+      Vi[IX(i)] = vn.im;
+      Xr[IX(i)] = x.re;
+      Xi[IX(i)] = x.im;
+    }
+    if (pl == (kp - 1) % DP) {  // the shifted row (diagonal entry h - lambda)
+      const int i = kp - 1;
+      const double hi = hcol[i];
+      const cplx v = mk(Vr[IX(i)], Vi[IX(i)]);
+      cplx x = mk(Xr[IX(i)], Xi[IX(i)]);
+      const cplx ri = csub(cmul(ccj, v), cmul(svc, csub(mk(hi, 0.0), mk(lre, lim))));
+      x = csub(x, cmul(xk, ri));
+      const double tre = hi - lre, tim = -lim;
+      const cplx vn = mk((cr * tre - ci * tim) + sv * v.re, (cr * tim + ci * tre) + sv * v.im);
       Vr[IX(i)] = vn.re;
       Vi[IX(i)] = vn.im;
       Xr[IX(i)] = x.re;
