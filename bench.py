@@ -67,12 +67,11 @@ def workload(cfg, seed=0, n_override=None):
 
 
 def partition(er, ec, rank, world):
-    """Cost-balanced shard: complex ~2.04x a real shift (flop model at n=16000)."""
-    if world == 1:
-        return er, ec
-    wr = np.array_split(er, world)[rank]
-    wc = np.array_split(ec, world)[rank]
-    return wr, wc
+    """This rank's shifts: an equal share of each kind (parallel.shard_bounds)."""
+    from paper_2101_05063_b200.parallel import shard_bounds
+
+    rc, cc = shard_bounds(er.size, ec.size, world)
+    return er[rc[rank]:rc[rank + 1]], ec[cc[rank]:cc[rank + 1]]
 
 
 class ClockSampler:

@@ -71,11 +71,13 @@ __device__ __forceinline__ double step1_apply(double x, double fb, double rr, do
 // ---- update steps 1-2 for one (tile row it < jt, shift q) ----
 // Step 1 (update_rupdate :211-231 / cupdate_crupdate :600-633).  bmax =
 // max|b| over the tile rows: exact for real columns; for complex columns
-// either the exact glibc-modulus maximum (bmax_exact) or an upper bound.
-// Returns false when a complex bound cannot prove the guard's result: the
-// caller then supplies the exact maximum and calls again.
+// either the exact glibc-modulus maximum (bmax_exact) or an upper bound, with
+// optionally a lower bound bmax_lo of the exact maximum.  Returns false when
+// the bounds cannot prove the guard's result: the caller then supplies the
+// exact maximum (or a tighter interval) and calls again.
 __device__ __forceinline__ bool scalars_step1(const Ctx& c, int jt, int it, int64_t q,
-                                              double bmax, bool bmax_exact, RowScalars& o) {
+                                              double bmax, bool bmax_exact, RowScalars& o,
+                                              double bmax_lo = -1.0) {
   const bool cplx = q < c.mc;
   const StepScalars st = c.SS[q];
   o.pad = 0;
@@ -98,11 +100,21 @@ __device__ __forceinline__ bool scalars_step1(const Ctx& c, int jt, int it, int6
   const double alam = shifted ? (cplx ? ghypot(lr, li) : fabs(lr)) : 0.0;
   const double hm0 = c.HM0[(int64_t)jt * c.N + it];
   const double arho = cplx ? ghypot(st.rho_re, st.rho_im) : fabs(st.rho_re);
+  int xe1;
   if (cplx && !bmax_exact) {
-    bmax *= BOUND_SLACK;
-    if (!protect_update_is_one(p2(g - be) * bmax, hm0 + alam, arho, omega)) return false;
+    if (!(bmax_lo >= 0.0)) bmax *= BOUND_SLACK;  // (interval mode: bmax is the upper end)
+    if (!protect_update_is_one(p2(g - be) * bmax, hm0 + alam, arho, omega)) {
+      // an interval [bmax_lo, bmax] around the exact maximum certifies the
+      // exponent when both ends agree (protect_update_e is monotone)
+      if (!(bmax_lo >= 0.0)) return false;
+      xe1 = protect_update_e(p2(g - be) * bmax_lo, hm0 + alam, arho, omega);
+      if (xe1 != protect_update_e(p2(g - be) * bmax, hm0 + alam, arho, omega)) return false;
+    } else {
+      xe1 = 0;
+    }
+  } else {
+    xe1 = protect_update_e(p2(g - be) * bmax, hm0 + alam, arho, omega);
   }
-  const int xe1 = protect_update_e(p2(g - be) * bmax, hm0 + alam, arho, omega);
   const int d = xe1 + g;
   o.fb = p2(d - be);
   o.fx = p2(d - ae);
@@ -226,10 +238,27 @@ __global__ void k_scalars(Ctx c, PanelArgs p, RowScalars* RSc) {
   double bmax = c.XB[(int64_t)it * c.ms + q];  // real: exact max|b|; complex: bound
   if (!scalars_step1(c, jt, it, q, bmax, !cplx, o)) {
     HSRQ_COUNT(9);
-    double m = 0.0;  // exact max |b| (rare: near overflow)
-    for (int r = 0; r < c.b_r; r++) m = fmax(m, ghypot(Xr[r], Xi[r]));
-    bmax = m;
-    scalars_step1(c, jt, it, q, bmax, true, o);
+    // near overflow: max|b| from scaled squared moduli (an interval of
+    // relative width 2^-47), glibc moduli only if that cannot decide
+    const bool pairs = ((c.ldx | c.b_r) & 1) == 0;
+    const int es = ilogb_pos(bmax * BOUND_SLACK);
+    const double sc = p2(-max(-1000, min(1020, es)));
+    double bm, tm;
+    seg_xprime_max<true>(Xr, Xi, Xr, c.b_r, pairs, 1.0, 0.0, 0.0, false, 0.0, 0.0, sc, bm, tm);
+    bool done = false;
+    if (es > -1000 && es < 1020 && tm >= 0x1p-960 && tm <= 16.0) {
+      const double qt = sqrt(tm);
+      const double lo = (qt - qt * 0x1p-47) * p2(es), hi = (qt + qt * 0x1p-47) * p2(es);
+      done = scalars_step1(c, jt, it, q, hi, false, o, lo);
+      if (done) bmax = hi;
+    }
+    if (!done) {
+      HSRQ_COUNT(12);
+      double m = 0.0;
+      for (int r = 0; r < c.b_r; r++) m = fmax(m, ghypot(Xr[r], Xi[r]));
+      bmax = m;
+      scalars_step1(c, jt, it, q, bmax, true, o);
+    }
   } else if (cplx) {
     bmax *= BOUND_SLACK;
   }

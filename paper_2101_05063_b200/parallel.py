@@ -15,35 +15,30 @@ import torch
 import torch.distributed as dist
 
 # flop-model ratio of a complex to a real shift at n=16000, b_r=128
-# (1.3330e9 / 6.5329e8, hessrq flops.py); used to balance the shards
+# (1.3330e9 / 6.5329e8, hessrq flops.py)
 COMPLEX_COST = 2.04
 
 
-def shard_bounds(n_real, n_cplx, world, cplx_cost=COMPLEX_COST):
-    """Contiguous cost-balanced cuts of the real-first sorted selection.
+def shard_bounds(n_real, n_cplx, world):
+    """Per-kind shard boundaries: ``(real_cuts, cplx_cuts)``, each ``world + 1`` long.
 
-    Returns ``world + 1`` boundaries into the sorted order (real shifts
-    first, then complex), each shard carrying ~1/world of the flop cost.
+    Every rank gets an equal share (to one shift) of the real AND of the
+    complex shifts, so the flop cost (complex ~2.04 x real at n=16000) and the
+    latency-bound diagonal sweeps of both kinds are balanced at once.
     """
-    cost = np.concatenate([np.ones(n_real), np.full(n_cplx, float(cplx_cost))])
-    csum = np.concatenate([[0.0], np.cumsum(cost)])
-    total = csum[-1]
-    cuts = [0]
-    for r in range(1, world):
-        cuts.append(int(np.searchsorted(csum, total * r / world, side="left")))
-    cuts.append(n_real + n_cplx)
-    cuts = np.maximum.accumulate(np.array(cuts))
-    return cuts
+    rc = np.array([(n_real * r) // world for r in range(world + 1)], dtype=np.int64)
+    cc = np.array([(n_cplx * r) // world for r in range(world + 1)], dtype=np.int64)
+    return rc, cc
 
 
-def local_selection(eigenvalues, rank, world, cplx_cost=COMPLEX_COST):
+def local_selection(eigenvalues, rank, world):
     """This rank's shifts (original indices, values) of a mixed selection."""
     eigs = np.asarray(eigenvalues, dtype=np.complex128).ravel()
     is_cplx = eigs.imag != 0.0
-    order = np.argsort(is_cplx, kind="stable")
-    cuts = shard_bounds(int(np.count_nonzero(~is_cplx)), int(np.count_nonzero(is_cplx)), world,
-                        cplx_cost)
-    idx = order[cuts[rank]:cuts[rank + 1]]
+    ridx = np.nonzero(~is_cplx)[0]
+    cidx = np.nonzero(is_cplx)[0]
+    rc, cc = shard_bounds(ridx.size, cidx.size, world)
+    idx = np.concatenate([ridx[rc[rank]:rc[rank + 1]], cidx[cc[rank]:cc[rank + 1]]])
     return idx, eigs[idx]
 
 

@@ -70,11 +70,10 @@ def test_first_failure_follows_reference_order():
 
 
 def test_shards_balance_flop_cost():
-    cuts = shard_bounds(3790, 6105, 8)
-    cost = np.concatenate([np.ones(3790), np.full(6105, 2.04)])
-    per = [cost[cuts[r]:cuts[r + 1]].sum() for r in range(8)]
-    assert cuts[0] == 0 and cuts[-1] == 9895
-    assert max(per) - min(per) <= 2.04 + 1e-9
+    rc, cc = shard_bounds(3790, 6105, 8)
+    assert rc[0] == cc[0] == 0 and rc[-1] == 3790 and cc[-1] == 6105
+    per = [(rc[r + 1] - rc[r]) + 2.04 * (cc[r + 1] - cc[r]) for r in range(8)]
+    assert max(per) - min(per) <= 1 + 2.04 + 1e-9
     eigs = np.concatenate([np.arange(5) + 0.5, np.arange(4) + 1j])
     seen = np.concatenate([local_selection(eigs, r, 3)[0] for r in range(3)])
     assert sorted(seen.tolist()) == list(range(9))
