@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_real(Ctx c, DiagArgs a) {
     if (pl == (kp % DP)) XX(kp) = xk;
     const double tau1 = ss * xk, tau2 = cc * xk;
     double nxm = 0.0, nvm = 0.0;
-#pragma unroll 4
+#pragma unroll 1
     for (int i = pl; i < kp - 1; i += DP) {
       const double hi = hcol[i];
       double vv = VV(i), xx = XX(i);
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
       const int ex = ilogb_pos(xb), er = ilogb_pos(rb);
       const double sx = p2(-max(-1000, min(1020, ex))), sr = p2(-max(-1000, min(1020, er)));
       double tx = 0.0, tr = 0.0;
-#pragma unroll 2
+#pragma unroll 1
       for (int i = pl; i < kp; i += DP) {
         const cplx t = i == kp - 1 ? csub(mk(hcol[i], 0.0), mk(lre, lim)) : mk(hcol[i], 0.0);
         const cplx ri = csub(cmul(ccj, mk(Vr[IX(i)], Vi[IX(i)])), cmul(svc, t));
@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
       Xi[IX(kp)] = xk.im;
     }
     double nxb = 0.0, nvb = 0.0;
-#pragma unroll 2
+#pragma unroll 1
     for (int i = pl; i < kp - 1; i += DP) {
       const double hi = hcol[i];
       const cplx v = mk(Vr[IX(i)], Vi[IX(i)]);
