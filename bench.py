@@ -156,6 +156,17 @@ def cpu_sample(h, er, ec, b_r, n_real=16, n_cplx=16, threads=None):
     return (sr.size + sc.size), dt, threads, f"{sr.size} real + {sc.size} complex shifts of the same H"
 
 
+def arm_config(cfg, n, m_r, m_c, b_r, world):
+    """The workload description both arms print (bench contract `config`)."""
+    return {
+        "workload": f"config{cfg}: n={n} random Hessenberg, {m_r} real + {m_c} complex shifts "
+                    f"({m_r + 2 * m_c} real columns), b_r={b_r}, one _solve_group attempt "
+                    f"(eigvec mode)",
+        "parallelism": f"shifts partitioned over {world} GPU(s), H replicated, NCCL gather of X",
+        "l2": "inputs (H, X: 2 GB each) exceed L2; no flush needed",
+    }
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -175,11 +186,12 @@ def run_reference(args):
     fl = F.reference_flops(n, b_r, min(args.cpu_real, er.size), min(args.cpu_cplx, ec.size))
     line = {
         "metric": METRIC, "impl": "reference", "value": v, "unit": "eigenvectors/s",
-        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded config-5 instance, LAPACK eigenvalues as shifts)",
-        "config": {"workload": f"config{args.config}: n={n}, b_r={b_r}, bounded CPU sample",
-                   "sample": sample},
+        "config": dict(arm_config(args.config, n, er.size, ec.size, b_r, args.gpus),
+                       cpu_sample=f"each step: {sample} on {threads} host threads (the CPU "
+                                  f"oracle port of the reference path; value in eigenvectors/s)"),
         "cpu_baseline": {"value": v, "unit": "eigenvectors/s", "cores": threads, "kind": "port",
                          "sample": sample, "tflops": fl / t / 1e12},
         "e2e": {"value": v, "unit": "eigenvectors/s", "h2d_bytes_per_step": 0,
@@ -379,13 +391,7 @@ def run_gpu(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded config-5 instance; shifts = LAPACK eigenvalues, cached in data/)",
-        "config": {
-            "workload": f"config{args.config}: n={n} random Hessenberg, {m_total_r} real + "
-                        f"{m_total_c} complex shifts ({m_total_r + 2 * m_total_c} real columns), "
-                        f"b_r={b_r}, one _solve_group attempt (eigvec mode)",
-            "parallelism": f"shifts partitioned over {world} GPU(s), H replicated, NCCL gather of X",
-            "l2": "inputs (H, X: 2 GB each) exceed L2; no flush needed",
-        },
+        "config": arm_config(args.config, n, m_total_r, m_total_c, b_r, world),
         "tflops": ref_fl / (ms / 1e3) / 1e12,
         "tflops_frac_of_fp64_peak": ref_fl / (ms / 1e3) / 1e12 / (peak * world),
         "executed_tflops": exe_fl / (ms / 1e3) / 1e12,
