@@ -13,6 +13,8 @@
  *                      the dhsrq3/chsrq3 engine backsolve.py:350-388.
  *                      Returns what SolutionBlock (core.py:251-260) carries:
  *                      x, per-column alpha, segment scales, represented norms.
+ *   hsrq_solve_group_host  the same seam with host (numpy) buffers, as
+ *                      _solve_group is called (inviter.py:127-133)
  *   hsrq_protect_update_batch   protect_update, _kernels/numba_backend.py:47-67
  *   hsrq_hypot_batch            libm hypot as bound by numba (every rotation)
  *   hsrq_tile_diag              reduce_diag + solve_rsolve (numba_backend.py:
@@ -112,6 +114,30 @@ int64_t hsrq_solve_group_async(const double* H, int64_t ldh, int64_t n, int32_t 
                                int64_t* fail, int32_t robust, int32_t mode, void* ws,
                                size_t ws_bytes, void* stream);
 int64_t hsrq_failure_count(void* ws, void* stream);
+
+/*
+ * Host-buffer variant of hsrq_solve_group -- the calling convention of the
+ * reference's _solve_group (numpy arrays in, SolutionBlock arrays out), for
+ * a ctypes / FFI binding without any device-array library.  Every pointer is
+ * HOST memory except dev_ws (device workspace of at least
+ * hsrq_host_workspace_bytes(n, b_r, m_cplx, m_real) bytes, reusable across
+ * calls).  H is copied to the device in column blocks from right to left on
+ * an internal copy stream, overlapped with the sweep (which consumes H in that
+ * order); use page-locked (pinned) host buffers for the overlap.  lam_im may
+ * be NULL when m_cplx == 0.  B as in hsrq_solve_group (b_broadcast = 1: one
+ * n-vector).  Outputs: X (n x ncol, ldx), seg_exp (N x (m_cplx + m_real)),
+ * alpha_exp, norms, log2norm, fail -- as hsrq_solve_group; the rotations stay
+ * on the device (the reference does not return them from _solve_group).
+ * Returns the number of failed shifts after synchronising `stream`, or a
+ * negative HSRQ_ERR_*.
+ */
+size_t hsrq_host_workspace_bytes(int64_t n, int32_t b_r, int64_t m_cplx, int64_t m_real);
+int64_t hsrq_solve_group_host(const double* H, int64_t ldh, int64_t n, int32_t b_r,
+                              const double* lam_re, const double* lam_im, int64_t m_cplx,
+                              int64_t m_real, const double* B, int64_t ldb, int32_t b_broadcast,
+                              double* X, int64_t ldx, int32_t* seg_exp, int32_t* alpha_exp,
+                              double* norms, double* log2norm, int64_t* fail, int32_t robust,
+                              int32_t mode, void* dev_ws, size_t dev_ws_bytes, void* stream);
 
 /* Guard-path event counters (diagnostics): out_host[16]; reset != 0 zeroes them. */
 int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset);

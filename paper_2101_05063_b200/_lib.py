@@ -34,6 +34,12 @@ SIGNATURES = {
          _p, _p, _p, _p, _p, _i32, _i32, _p, _sz, _p],
     ),
     "hsrq_failure_count": (_i64, [_p, _p]),
+    "hsrq_host_workspace_bytes": (_sz, [_i64, _i32, _i64, _i64]),
+    "hsrq_solve_group_host": (
+        _i64,
+        [_p, _i64, _i64, _i32, _p, _p, _i64, _i64, _p, _i64, _i32, _p, _i64, _p, _p, _p, _p, _p,
+         _i32, _i32, _p, _sz, _p],
+    ),
     "hsrq_last_launch_count": (_i64, []),
     "hsrq_set_timing": (None, [_i32]),
     "hsrq_phase_times": (None, [_p]),

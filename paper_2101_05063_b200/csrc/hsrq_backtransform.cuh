@@ -11,10 +11,11 @@
 constexpr int BT_WARPS = 4;
 
 __global__ void __launch_bounds__(BT_WARPS * 32) k_backtransform(Ctx c, int32_t* alpha_exp,
-                                                                 double* norms, double* log2norm) {
+                                                                 double* norms, double* log2norm,
+                                                                 int64_t q_begin, int64_t q_end) {
   const int lane = threadIdx.x & 31;
-  const int64_t q = (int64_t)blockIdx.x * BT_WARPS + (threadIdx.x >> 5);
-  if (q >= c.ms) return;
+  const int64_t q = q_begin + (int64_t)blockIdx.x * BT_WARPS + (threadIdx.x >> 5);
+  if (q >= q_end) return;
   bool cplx;
   int64_t col;
   col_of_shift(c, q, cplx, col);

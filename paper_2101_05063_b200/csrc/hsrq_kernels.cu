@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 #include <cstdint>
 #include <cstdio>
 #include <cmath>
@@ -147,6 +148,35 @@ __global__ void k_hmk(Ctx c) {
   c.HMK[(int64_t)jt * MAXK + kp] = m;
 }
 
+// The tables of one tile column jt (host-feed mode, where H arrives column
+// block by column block): HM0[jt][*] / RS[jt][*] as k_tables (blocks over the
+// rows < js) and HMK[jt][*] as k_hmk (the last block).
+__global__ void k_tables_jt(Ctx c, int jt) {
+  const int64_t js = (int64_t)jt * c.b_r;
+  const int64_t je = js + c.b_r < c.n ? js + c.b_r : c.n;
+  const int k = (int)(je - js);
+  if (blockIdx.x == gridDim.x - 1) {  // HMK
+    for (int kp = threadIdx.x; kp < MAXK; kp += blockDim.x) {
+      if (kp < 1 || kp >= k) continue;
+      double m = 0.0;
+      for (int i = 0; i < kp; i++) {
+        const double v = fabs(c.H[(js + kp - 1) * c.ldh + js + i]);
+        if (v > m) m = v;
+      }
+      c.HMK[(int64_t)jt * MAXK + kp] = m;
+    }
+    return;
+  }
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (jt < 1 || r >= js) return;
+  const int i = (int)(r / c.b_r);
+  const double h0 = fabs(c.H[(js - 1) * c.ldh + r]);
+  double acc = 0.0;
+  for (int j = 1; j < k; j++) acc += fabs(c.H[(js - 1 + j) * c.ldh + r]);
+  atomicMax((unsigned long long*)&c.HM0[(int64_t)jt * c.N + i], dkey(h0));
+  atomicMax((unsigned long long*)&c.RS[(int64_t)jt * c.N + i], dkey(acc));
+}
+
 // X = B (or the broadcast start vector), Cr(:, N-1) = H(:, n-1) - lambda e_n
 // (reduce.py:66-69, 77-78).
 __global__ void k_init(Ctx c, const double* B, int64_t ldb, int b_broadcast) {
@@ -168,7 +198,7 @@ __global__ void k_init(Ctx c, const double* B, int64_t ldb, int b_broadcast) {
   c.Cr[col * c.ldx + r] = h;
 }
 
-__global__ void k_zero_state(Ctx c) {
+__global__ void k_zero_state(Ctx c, int zero_tables) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t ne = (int64_t)c.N * c.ms;
   if (t < ne) {
@@ -176,7 +206,7 @@ __global__ void k_zero_state(Ctx c) {
     c.XB[t] = 0.0;
   }
   if (t < c.ms) c.fail[t] = 0;
-  if (t < (int64_t)c.N * c.N) {
+  if (zero_tables && t < (int64_t)c.N * c.N) {
     c.HM0[t] = 0.0;
     c.RS[t] = 0.0;
   }
@@ -336,12 +366,26 @@ WsLayout ws_layout(int64_t n, int b_r, int64_t mc, int64_t mr) {
   return L;
 }
 
+// Host-feed mode (hsrq_solve_group_host): H is copied from host memory on a
+// copy stream in column blocks, right to left -- the order the sweep
+// consumes it -- so the transfer overlaps the sweep.  Block b holds columns
+// [b*b_r - 1, (b+1)*b_r - 1) (block N: the rest); blk[b] is recorded when it
+// has landed.  Tile column jt needs blocks jt..N.
+struct HostFeed {
+  const double* H_host;  // column-major, leading dimension ldh_host
+  int64_t ldh_host;
+  double* X_host;        // solution destination (column-major, ldx_host), or null
+  int64_t ldx_host;
+  cudaStream_t copy;     // copy stream (also runs the per-block table kernels)
+  cudaEvent_t* blk;      // N + 2 events: blk[b] = block b copied and tabulated; blk[N + 1] entry
+};
+
 int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const double* lam_re,
                    const double* lam_im, int64_t mc, int64_t mr, const double* B, int64_t ldb,
                    int32_t b_broadcast, double* X, int64_t ldx, double* c_re, double* c_im,
                    double* s, int64_t ldc, int32_t* seg_exp, int32_t* alpha_exp, double* norms,
                    double* log2norm, int64_t* fail, int32_t robust, int32_t mode, void* ws,
-                   size_t ws_bytes, cudaStream_t stream) {
+                   size_t ws_bytes, cudaStream_t stream, const HostFeed* feed = nullptr) {
   g_launches = 0;
   if (n < 1 || b_r < 1 || b_r > MAXK || b_r > n || mc < 0 || mr < 0 || mc + mr < 1 || ldx < n ||
       ldh < n || ldc < n) {
@@ -427,18 +471,50 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     cudaEventRecord(ev[0], stream);
   }
   const int64_t nzero = std::max<int64_t>((int64_t)c.N * c.ms, (int64_t)c.N * c.N) + c.ms + 1;
-  k_zero_state<<<(unsigned)((nzero + 255) / 256), 256, 0, stream>>>(c);
+  k_zero_state<<<(unsigned)((nzero + 255) / 256), 256, 0, stream>>>(c, feed ? 0 : 1);
   g_launches++;
   const int64_t nbop = 2 * c.ncol_pad * KP;
   k_zero_bop<<<(unsigned)((nbop + 255) / 256), 256, 0, stream>>>(c.Bop, nbop);
   g_launches++;
-  if (c.N > 1) {
-    dim3 gt((unsigned)((n + 255) / 256), (unsigned)(c.N - 1));
-    k_tables<<<gt, 256, 0, stream>>>(c);
+  if (!feed) {
+    if (c.N > 1) {
+      dim3 gt((unsigned)((n + 255) / 256), (unsigned)(c.N - 1));
+      k_tables<<<gt, 256, 0, stream>>>(c);
+      g_launches++;
+    }
+    k_hmk<<<(unsigned)c.N, MAXK, 0, stream>>>(c);
     g_launches++;
+  } else {
+    // H arrives block by block on the copy stream (after prior work on
+    // `stream` released the buffers); each block's table kernel follows its
+    // copy there, off the sweep's critical path
+    cudaStream_t cp = feed->copy;
+    cudaEventRecord(feed->blk[c.N + 1], stream);
+    cudaStreamWaitEvent(cp, feed->blk[c.N + 1], 0);
+    if (!ck(cudaMemsetAsync(c.HM0, 0, sizeof(double) * (size_t)c.N * c.N, cp), "memset") ||
+        !ck(cudaMemsetAsync(c.RS, 0, sizeof(double) * (size_t)c.N * c.N, cp), "memset"))
+      return HSRQ_ERR_CUDA;
+    for (int64_t b = c.N; b >= 0; --b) {
+      const int64_t c0 = std::min<int64_t>(n, std::max<int64_t>(0, b * b_r - 1));
+      const int64_t c1 = b == c.N ? n : std::min<int64_t>(n, (b + 1) * b_r - 1);
+      if (c1 > c0 &&
+          !ck(cudaMemcpy2DAsync(const_cast<double*>(H) + c0 * ldh, sizeof(double) * ldh,
+                                feed->H_host + c0 * feed->ldh_host,
+                                sizeof(double) * feed->ldh_host, sizeof(double) * n,
+                                (size_t)(c1 - c0), cudaMemcpyHostToDevice, cp),
+              "H2D H"))
+        return HSRQ_ERR_CUDA;
+      if (b < c.N) {
+        const unsigned nb = (unsigned)((b * b_r + 255) / 256) + 1;
+        k_tables_jt<<<nb, 256, 0, cp>>>(c, (int)b);
+        g_launches++;
+      }
+      cudaEventRecord(feed->blk[b], cp);
+    }
+    // k_init needs column n - 1
+    cudaStreamWaitEvent(stream, feed->blk[c.N], 0);
+    cudaStreamWaitEvent(stream, feed->blk[c.N - 1], 0);
   }
-  k_hmk<<<(unsigned)c.N, MAXK, 0, stream>>>(c);
-  g_launches++;
   {
     dim3 gi((unsigned)((n + 255) / 256), (unsigned)c.ncol);
     k_init<<<gi, 256, 0, stream>>>(c, B, ldb, b_broadcast);
@@ -472,6 +548,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     int64_t je = a.js + b_r < n ? a.js + b_r : n;
     a.k = (int)(je - a.js);
     a.has_left = jt > 0;
+    if (feed) cudaStreamWaitEvent(stream, feed->blk[jt], 0);  // this column's H block + tables
     // Real and complex shifts are independent columns: their diagonal
     // kernels run concurrently (the real one on a side stream, forked and
     // joined with events), so the latency-bound sweeps share the SMs.
@@ -527,9 +604,45 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
       cudaEventRecord(ev[4 + 3 * jt], stream);
     }
   }
-  k_backtransform<<<(unsigned)((c.ms + BT_WARPS - 1) / BT_WARPS), BT_WARPS * 32, 0, stream>>>(
-      c, alpha_exp, norms, log2norm);
-  g_launches++;
+  if (!feed || !feed->X_host) {
+    k_backtransform<<<(unsigned)((c.ms + BT_WARPS - 1) / BT_WARPS), BT_WARPS * 32, 0, stream>>>(
+        c, alpha_exp, norms, log2norm, 0, c.ms);
+    g_launches++;
+  } else {
+    // host feed: backtransform in shift chunks; each chunk's columns of X go
+    // to the host on the copy stream while the next chunk is transformed
+    const int nch = 8;
+    for (int ch = 0; ch < nch; ch++) {
+      const int64_t q0 = c.ms * ch / nch, q1 = c.ms * (ch + 1) / nch;
+      if (q1 <= q0) continue;
+      k_backtransform<<<(unsigned)((q1 - q0 + BT_WARPS - 1) / BT_WARPS), BT_WARPS * 32, 0,
+                        stream>>>(c, alpha_exp, norms, log2norm, q0, q1);
+      g_launches++;
+      // (the block events are free again: every wait on them is already enqueued)
+      cudaEvent_t e = feed->blk[ch % (c.N + 1)];
+      cudaEventRecord(e, stream);
+      cudaStreamWaitEvent(feed->copy, e, 0);
+      // columns of shifts [q0, q1): complex part then real part
+      const int64_t cq1 = std::min<int64_t>(q1, c.mc), rq0 = std::max<int64_t>(q0, c.mc);
+      if (cq1 > q0 &&
+          !ck(cudaMemcpy2DAsync(feed->X_host + 2 * q0 * feed->ldx_host,
+                                sizeof(double) * feed->ldx_host, c.X + 2 * q0 * c.ldx,
+                                sizeof(double) * c.ldx, sizeof(double) * n,
+                                (size_t)(2 * (cq1 - q0)), cudaMemcpyDeviceToHost, feed->copy),
+              "D2H X"))
+        return HSRQ_ERR_CUDA;
+      if (q1 > rq0 &&
+          !ck(cudaMemcpy2DAsync(feed->X_host + (2 * c.mc + rq0 - c.mc) * feed->ldx_host,
+                                sizeof(double) * feed->ldx_host,
+                                c.X + (2 * c.mc + rq0 - c.mc) * c.ldx, sizeof(double) * c.ldx,
+                                sizeof(double) * n, (size_t)(q1 - rq0), cudaMemcpyDeviceToHost,
+                                feed->copy),
+              "D2H X"))
+        return HSRQ_ERR_CUDA;
+    }
+    cudaEventRecord(feed->blk[c.N + 1], feed->copy);
+    cudaStreamWaitEvent(stream, feed->blk[c.N + 1], 0);  // X is on the host
+  }
   if (g_timing) {
     cudaEventRecord(ev[nev - 2], stream);
     cudaEventSynchronize(ev[nev - 2]);
@@ -560,6 +673,38 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   return 0;
 }
 
+// Device workspace of the host-buffer entry point (hsrq_solve_group_host).
+struct HostLayout {
+  int64_t ldh;  // device H leading dimension (even)
+  size_t h, x, cre, cim, s, lre, lim, b, seg, aexp, norms, l2, fail, ws, total;
+};
+HostLayout host_layout(int64_t n, int b_r, int64_t mc, int64_t mr) {
+  HostLayout L;
+  const int64_t ncol = 2 * mc + mr, ms = mc + mr, N = (n + b_r - 1) / b_r;
+  L.ldh = n + (n & 1);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = off;
+    off = align_up(off + bytes, 256);
+    return at;
+  };
+  L.h = take(sizeof(double) * (size_t)L.ldh * n);
+  L.x = take(sizeof(double) * (size_t)n * ncol);
+  L.cre = take(sizeof(double) * (size_t)n * ms);
+  L.cim = take(sizeof(double) * (size_t)n * ms);
+  L.s = take(sizeof(double) * (size_t)n * ms);
+  L.lre = take(sizeof(double) * (size_t)ms);
+  L.lim = take(sizeof(double) * (size_t)ms);
+  L.b = take(sizeof(double) * (size_t)n);
+  L.seg = take(sizeof(int32_t) * (size_t)N * ms);
+  L.aexp = take(sizeof(int32_t) * (size_t)ms);
+  L.norms = take(sizeof(double) * (size_t)ms);
+  L.l2 = take(sizeof(double) * (size_t)ms);
+  L.fail = take(sizeof(int64_t) * (size_t)ms);
+  L.ws = take(ws_layout(n, b_r, mc, mr).total);
+  L.total = off;
+  return L;
+}
 }  // namespace
 
 extern "C" {
@@ -612,6 +757,108 @@ int64_t hsrq_solve_group(const double* H, int64_t ldh, int64_t n, int32_t b_r,
           "copy nfail"))
     return HSRQ_ERR_CUDA;
   if (!ck(cudaStreamSynchronize((cudaStream_t)stream), "sync")) return HSRQ_ERR_CUDA;
+  return (int64_t)nf;
+}
+
+size_t hsrq_host_workspace_bytes(int64_t n, int32_t b_r, int64_t m_cplx, int64_t m_real) {
+  if (n < 1 || b_r < 1) return 0;
+  return host_layout(n, b_r, m_cplx, m_real).total;
+}
+
+int64_t hsrq_solve_group_host(const double* H, int64_t ldh, int64_t n, int32_t b_r,
+                              const double* lam_re, const double* lam_im, int64_t m_cplx,
+                              int64_t m_real, const double* B, int64_t ldb, int32_t b_broadcast,
+                              double* X, int64_t ldx, int32_t* seg_exp, int32_t* alpha_exp,
+                              double* norms, double* log2norm, int64_t* fail, int32_t robust,
+                              int32_t mode, void* dev_ws, size_t dev_ws_bytes, void* stream_) {
+  if (n < 1 || b_r < 1 || b_r > MAXK || b_r > n || m_cplx < 0 || m_real < 0 ||
+      m_cplx + m_real < 1 || ldh < n || ldx < n || (!b_broadcast && ldb < n)) {
+    snprintf(g_err, sizeof(g_err), "bad configuration (n=%lld b_r=%d)", (long long)n, b_r);
+    return HSRQ_ERR_CONFIG;
+  }
+  const HostLayout L = host_layout(n, b_r, m_cplx, m_real);
+  if (dev_ws_bytes < L.total) return HSRQ_ERR_WORKSPACE;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  unsigned char* w = (unsigned char*)dev_ws;
+  double* Hd = (double*)(w + L.h);
+  double* Xd = (double*)(w + L.x);
+  const int64_t ms = m_cplx + m_real, ncol = 2 * m_cplx + m_real, N = (n + b_r - 1) / b_r;
+  // per-thread copy stream and event pool (N + 2 events)
+  thread_local cudaStream_t copy = nullptr;
+  thread_local int copy_dev = -1;
+  thread_local std::vector<cudaEvent_t> evs;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (copy_dev != dev) {
+    if (!ck(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "copy stream"))
+      return HSRQ_ERR_CUDA;
+    for (auto e : evs) cudaEventDestroy(e);
+    evs.clear();
+    copy_dev = dev;
+  }
+  while ((int64_t)evs.size() < N + 2) {
+    cudaEvent_t e;
+    if (!ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event")) return HSRQ_ERR_CUDA;
+    evs.push_back(e);
+  }
+  // shifts and right-hand sides on the compute stream
+  double* lre = (double*)(w + L.lre);
+  double* lim = (double*)(w + L.lim);
+  if (!ck(cudaMemcpyAsync(lre, lam_re, sizeof(double) * ms, cudaMemcpyHostToDevice, stream),
+          "H2D lam"))
+    return HSRQ_ERR_CUDA;
+  if (lam_im) {
+    if (!ck(cudaMemcpyAsync(lim, lam_im, sizeof(double) * ms, cudaMemcpyHostToDevice, stream),
+            "H2D lam"))
+      return HSRQ_ERR_CUDA;
+  } else if (!ck(cudaMemsetAsync(lim, 0, sizeof(double) * ms, stream), "memset lam")) {
+    return HSRQ_ERR_CUDA;
+  }
+  const double* Bd;
+  int64_t ldbd;
+  if (b_broadcast) {
+    double* bd = (double*)(w + L.b);
+    if (!ck(cudaMemcpyAsync(bd, B, sizeof(double) * n, cudaMemcpyHostToDevice, stream), "H2D B"))
+      return HSRQ_ERR_CUDA;
+    Bd = bd;
+    ldbd = 0;
+  } else {  // B lands in X (k_init reads and writes each entry in one thread)
+    if (!ck(cudaMemcpy2DAsync(Xd, sizeof(double) * n, B, sizeof(double) * ldb,
+                              sizeof(double) * n, (size_t)ncol, cudaMemcpyHostToDevice, stream),
+            "H2D B"))
+      return HSRQ_ERR_CUDA;
+    Bd = Xd;
+    ldbd = n;
+  }
+  HostFeed feed{H, ldh, X, ldx, copy, evs.data()};
+  int32_t* segd = (int32_t*)(w + L.seg);
+  int32_t* aexpd = (int32_t*)(w + L.aexp);
+  double* normsd = (double*)(w + L.norms);
+  double* l2d = (double*)(w + L.l2);
+  int64_t* faild = (int64_t*)(w + L.fail);
+  void* wsd = w + L.ws;
+  const int64_t r = solve_impl(Hd, L.ldh, n, b_r, lre, lim, m_cplx, m_real, Bd, ldbd, b_broadcast,
+                               Xd, n, (double*)(w + L.cre), (double*)(w + L.cim),
+                               (double*)(w + L.s), n, segd, aexpd, normsd, l2d, faild, robust, mode,
+                               wsd, ws_layout(n, b_r, m_cplx, m_real).total, stream, &feed);
+  if (r < 0) return r;
+  unsigned long long nf = 0;
+  const WsLayout WL = ws_layout(n, b_r, m_cplx, m_real);
+  if (!ck(cudaMemcpyAsync(seg_exp, segd, sizeof(int32_t) * N * ms, cudaMemcpyDeviceToHost, stream),
+          "D2H seg") ||
+      !ck(cudaMemcpyAsync(alpha_exp, aexpd, sizeof(int32_t) * ms, cudaMemcpyDeviceToHost, stream),
+          "D2H alpha") ||
+      !ck(cudaMemcpyAsync(norms, normsd, sizeof(double) * ms, cudaMemcpyDeviceToHost, stream),
+          "D2H norms") ||
+      !ck(cudaMemcpyAsync(log2norm, l2d, sizeof(double) * ms, cudaMemcpyDeviceToHost, stream),
+          "D2H log2norm") ||
+      !ck(cudaMemcpyAsync(fail, faild, sizeof(int64_t) * ms, cudaMemcpyDeviceToHost, stream),
+          "D2H fail") ||
+      !ck(cudaMemcpyAsync(&nf, (unsigned char*)wsd + WL.nfail, sizeof(nf), cudaMemcpyDeviceToHost,
+                          stream),
+          "D2H nfail") ||
+      !ck(cudaStreamSynchronize(stream), "sync"))
+    return HSRQ_ERR_CUDA;
   return (int64_t)nf;
 }
 

@@ -147,6 +147,98 @@ class GroupSolver:
                            int(self.lib.hsrq_last_launch_count()))
 
 
+@dataclass
+class HostOutput:
+    """Host-side results of one solve group through hsrq_solve_group_host."""
+
+    X: np.ndarray          # (ncol, n): row c = column c
+    seg_exp: np.ndarray    # (N, ms) int32
+    alpha_exp: np.ndarray  # (ms,) int32
+    norms: np.ndarray
+    log2norm: np.ndarray
+    fail: np.ndarray       # (ms,) int64
+    nfail: int
+    mc: int
+    mr: int
+
+
+class HostGroupSolver:
+    """hsrq_solve_group_host: host (numpy, ideally pinned) buffers in and out.
+
+    The reference's own calling convention for the seam -- ``_solve_group``
+    takes and returns numpy arrays (inviter.py:91-106); only the reusable
+    device workspace is a device allocation.  H streams to the device in
+    column blocks overlapped with the sweep (include/hsrq.h).
+    """
+
+    def __init__(self, n, b_r, m_cplx, m_real, device=None):
+        if not (1 <= b_r <= n):
+            raise ConfigError(f"tile size b_r={b_r} out of range for n={n}")
+        if b_r > MAX_TILE:
+            raise ConfigError(f"the B200 path supports b_r <= {MAX_TILE} (got {b_r})")
+        self.lib = _lib.load()
+        self.n, self.b_r, self.mc, self.mr = int(n), int(b_r), int(m_cplx), int(m_real)
+        self.ms = self.mc + self.mr
+        self.ncol = 2 * self.mc + self.mr
+        self.N = (self.n + self.b_r - 1) // self.b_r
+        self.device = device or default_device()
+        self.ws_bytes = int(self.lib.hsrq_host_workspace_bytes(self.n, self.b_r, self.mc, self.mr))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+
+    def launch(self, h, lam_re, lam_im, b, broadcast, out, robust=True, mode="eigvec",
+               stream=None):
+        """h: (n, n) float64 column-major (Fortran) array; lam_*: (ms,) complex-first;
+        b: (n,) start vector (broadcast) or (ncol, n) rows = columns; out: HostOutput."""
+        h = np.asarray(h)
+        if not (h.flags.f_contiguous and h.dtype == np.float64):
+            h = np.asfortranarray(h, dtype=np.float64)
+        stream = stream or torch.cuda.current_stream(self.device)
+        P = lambda a: ctypes.c_void_p(a.ctypes.data) if a is not None else ctypes.c_void_p(0)
+        mode_i = {"solve": 0, "eigvec": 1}[mode]
+        r = self.lib.hsrq_solve_group_host(
+            P(h), h.shape[0], self.n, self.b_r, P(lam_re), P(lam_im), self.mc, self.mr, P(b),
+            0 if broadcast else self.n, 1 if broadcast else 0, P(out.X), self.n, P(out.seg_exp),
+            P(out.alpha_exp), P(out.norms), P(out.log2norm), P(out.fail), int(bool(robust)),
+            mode_i, _ptr(self.ws), self.ws_bytes, ctypes.c_void_p(stream.cuda_stream))
+        if r < 0:
+            raise RuntimeError(f"hsrq_solve_group_host failed ({r}): {_lib.last_error()}")
+        out.nfail = int(r)
+        return out
+
+    def new_output(self, pinned=False):
+        def alloc(shape, dtype):
+            if pinned:
+                return torch.empty(shape, dtype=dtype).pin_memory().numpy()
+            return np.empty(shape, dtype=torch.empty(0, dtype=dtype).numpy().dtype)
+
+        return HostOutput(X=alloc((self.ncol, self.n), torch.float64),
+                          seg_exp=alloc((self.N, self.ms), torch.int32),
+                          alpha_exp=alloc((self.ms,), torch.int32),
+                          norms=alloc((self.ms,), torch.float64),
+                          log2norm=alloc((self.ms,), torch.float64),
+                          fail=alloc((self.ms,), torch.int64), nfail=0, mc=self.mc, mr=self.mr)
+
+
+def solve_group_host(h, eigs_cplx, eigs_real, b, b_r, *, robust=True, mode="eigvec",
+                     device=None):
+    """One solve group through the host-buffer entry point; returns HostOutput."""
+    hm = h if isinstance(h, HessenbergMatrix) else HessenbergMatrix(h)
+    _check_h(hm)
+    mc = len(np.atleast_1d(eigs_cplx)) if eigs_cplx is not None else 0
+    mr = len(np.atleast_1d(eigs_real)) if eigs_real is not None else 0
+    hs = HostGroupSolver(hm.n, b_r, mc, mr, device)
+    lam = np.concatenate([np.asarray(eigs_cplx if mc else [], dtype=np.complex128).ravel(),
+                          np.asarray(eigs_real if mr else [], dtype=np.float64).ravel()
+                          .astype(np.complex128)])
+    bb = np.ascontiguousarray(b, dtype=np.float64)
+    broadcast = bb.ndim == 1
+    if not broadcast and bb.shape == (hm.n, hs.ncol):
+        bb = np.ascontiguousarray(bb.T)
+    out = hs.new_output()
+    return hs.launch(np.asfortranarray(hm.data), np.ascontiguousarray(lam.real),
+                     np.ascontiguousarray(lam.imag), bb, broadcast, out, robust=robust, mode=mode)
+
+
 def _check_h(hm):
     if not hm.is_unreduced():
         raise ConfigError("matrix must be unreduced (nonzero subdiagonal)")

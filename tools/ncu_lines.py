@@ -19,11 +19,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2101_05063_b200", "libhsrq_b200.so")
 
 
-def sass_lines(func_pat):
+def sass_lines(func_pat, outer=False):
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", LIB], cwd=tmp, check=True, capture_output=True)
     cubin = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-    out = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cubin)], check=True,
+    out = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cubin)], check=True,
                          capture_output=True, text=True).stdout.split("\n")
     start = [i for i, l in enumerate(out) if l.startswith(".text.") and re.search(func_pat, l)]
     if not start:
@@ -32,9 +32,10 @@ def sass_lines(func_pat):
     i1 = next((i for i in range(i0 + 1, len(out)) if out[i].startswith(".text.")), len(out))
     cur, m2l = None, {}
     for l in out[i0:i1]:
-        m = re.search(r'//## File "([^"]+)", line (\d+)', l)
-        if m:
-            cur = (os.path.basename(m.group(1)), int(m.group(2)))
+        if l.strip().startswith("//## File"):
+            locs = re.findall(r'"([^"]+)", line (\d+)', l)
+            f, ln = locs[-1] if outer else locs[0]
+            cur = (os.path.basename(f), int(ln))
             continue
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", l)
         if m and cur:
@@ -48,6 +49,8 @@ def main():
     ap.add_argument("kernel", help="regex of the kernel name as ncu shows it")
     ap.add_argument("func", help="regex of the mangled SASS function name")
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--outer", action="store_true",
+                    help="attribute inlined code to its outermost call site")
     a = ap.parse_args()
     txt = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--kernel-name",
                           f"regex:{a.kernel}"], check=True, capture_output=True, text=True).stdout
@@ -55,7 +58,7 @@ def main():
     hi = [i for i, r in enumerate(rows) if len(r) > 3 and r[0] == "Address"][0]
     h = rows[hi]
     ix = {k: i for i, k in enumerate(h)}
-    m2l = sass_lines(a.func)
+    m2l = sass_lines(a.func, a.outer)
     agg = collections.defaultdict(lambda: [0.0, 0.0])
     base = None
     ti = ts = 0.0
