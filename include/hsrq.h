@@ -170,6 +170,22 @@ int64_t hsrq_tile_diag(int32_t k, int32_t b, const double* hdiag, const double* 
                        int32_t* beta_exp, int64_t* status, int32_t robust, double omega,
                        void* stream);
 
+/*
+ * hsrq_tile_backtransform: rbacktransform / crbacktransform
+ * (numba_backend.py:326-375, :759-822) on b columns of length n with tiles of
+ * b_r rows -- the tile-level operator API of the backtransform kernel.
+ *   c_re, c_im, s  b x n (row q = shift q's rotations, row i mixing i-1 and i);
+ *                  c_im ignored unless cplx
+ *   seg_exp        N x b int32 row-major by tile: alpha = 2^seg_exp
+ *   x              in/out, column-major n x b (real) or n x 2b (re, im columns)
+ *   norms, alpha_exp  out, b entries (the reference's norms_out / alpha_out)
+ *   mode           1 = eigvec (normalise), 0 = solve (omega guard)
+ */
+int64_t hsrq_tile_backtransform(int64_t n, int32_t b_r, int32_t b, int32_t cplx,
+                                const double* c_re, const double* c_im, const double* s,
+                                const int32_t* seg_exp, double* x, double* norms,
+                                int32_t* alpha_exp, int32_t mode, double omega, void* stream);
+
 /* Elementwise device evaluations for bit-level parity of the scalar helpers. */
 int64_t hsrq_protect_update_batch(const double* bnorm, const double* hnorm, const double* xnorm,
                                   double omega, int64_t count, double* out, void* stream);

@@ -411,9 +411,9 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   c.X = X;
   c.ldx = ldx;
   c.Cr = (double*)(w + L.cr);
-  c.c_re = c_re;
-  c.c_im = c_im;
-  c.s = s;
+  c.c_re = const_cast<double*>(c_re);
+  c.c_im = const_cast<double*>(c_im);
+  c.s = const_cast<double*>(s);
   c.ldc = ldc;
   c.E = seg_exp;
   c.Bop = (double*)(w + L.bop);
@@ -924,6 +924,47 @@ int64_t hsrq_tile_diag(int32_t k, int32_t b, const double* hdiag, const double* 
   diag_launch(lam_im != nullptr, c, a, (cudaStream_t)stream);
   if (!ck(cudaGetLastError(), "launch") || !ck(cudaStreamSynchronize((cudaStream_t)stream), "sync"))
     return HSRQ_ERR_CUDA;
+  return 0;
+}
+
+int64_t hsrq_tile_backtransform(int64_t n, int32_t b_r, int32_t b, int32_t cplx,
+                                const double* c_re, const double* c_im, const double* s,
+                                const int32_t* seg_exp, double* x, double* norms,
+                                int32_t* alpha_exp, int32_t mode, double omega, void* stream_) {
+  if (n < 1 || b_r < 1 || b < 1) return HSRQ_ERR_CONFIG;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  Ctx c;
+  memset(&c, 0, sizeof(c));
+  c.n = n;
+  c.b_r = b_r;
+  c.N = (int)((n + b_r - 1) / b_r);
+  c.mc = cplx ? b : 0;
+  c.mr = cplx ? 0 : b;
+  c.ms = b;
+  c.ncol = cplx ? 2 * b : b;
+  c.X = x;
+  c.ldx = n;
+  c.c_re = const_cast<double*>(c_re);
+  c.c_im = const_cast<double*>(c_im);
+  c.s = const_cast<double*>(s);
+  c.ldc = n;
+  c.E = const_cast<int32_t*>(seg_exp);
+  c.robust = 1;
+  c.mode = mode;
+  c.omega = omega;
+  int64_t* fail = nullptr;
+  double* l2 = nullptr;
+  if (!ck(cudaMallocAsync(&fail, sizeof(int64_t) * b, stream), "alloc") ||
+      !ck(cudaMallocAsync(&l2, sizeof(double) * b, stream), "alloc") ||
+      !ck(cudaMemsetAsync(fail, 0, sizeof(int64_t) * b, stream), "memset"))
+    return HSRQ_ERR_CUDA;
+  c.fail = fail;
+  k_backtransform<<<(unsigned)((b + BT_WARPS - 1) / BT_WARPS), BT_WARPS * 32, 0, stream>>>(
+      c, alpha_exp, norms, l2, 0, b);
+  const bool ok = ck(cudaGetLastError(), "launch");
+  cudaFreeAsync(fail, stream);
+  cudaFreeAsync(l2, stream);
+  if (!ok || !ck(cudaStreamSynchronize(stream), "sync")) return HSRQ_ERR_CUDA;
   return 0;
 }
 

@@ -221,3 +221,30 @@ def test_config1_matches_reference(dev):
         assert np.linalg.norm(_phase_align(x, vr[:, l]) - vr[:, l]) <= 1e-8
         res = np.linalg.norm(h @ x - shifts[l] * x) / (hf * np.linalg.norm(x))
         assert res <= 10 * n * eps
+
+
+def test_tile_backtransform_bitwise(dev):
+    """rbacktransform / crbacktransform (numba_backend.py:326-375, :759-822) == the
+    k_backtransform kernel through hsrq_tile_backtransform, bit for bit: consistency
+    scaling, two-pass norm, normalise (eigvec) or omega guard (solve), rotation
+    sweep, zero columns."""
+    from paper_2101_05063_b200 import _lib
+
+    L = _lib.load()
+    g = golden("backtransform")
+    for t in g["tags"]:
+        n, b_r, b, cplx, mode = (int(v) for v in g[f"{t}_meta"])
+        cre = _d(g[f"{t}_cre"].T, dev)  # (b, n): row q = shift q
+        cim = _d(g[f"{t}_cim"].T, dev)
+        s = _d(g[f"{t}_s"].T, dev)
+        seg = _d(g[f"{t}_seg"], dev, torch.int32)
+        x = _d(g[f"{t}_x"].T, dev)  # column-major n x (b or 2b)
+        norms = torch.empty(b, dtype=torch.float64, device=dev)
+        aexp = torch.empty(b, dtype=torch.int32, device=dev)
+        r = L.hsrq_tile_backtransform(n, b_r, b, cplx, _p(cre), _p(cim), _p(s), _p(seg), _p(x),
+                                      _p(norms), _p(aexp), mode, float(g[f"{t}_omega"]),
+                                      torch.cuda.current_stream().cuda_stream)
+        assert r == 0, _lib.last_error()
+        assert np.array_equal(x.cpu().numpy().T, g[f"{t}_xout"]), t
+        assert np.array_equal(norms.cpu().numpy(), g[f"{t}_norms"]), t
+        assert np.array_equal(np.ldexp(1.0, aexp.cpu().numpy()), g[f"{t}_alpha"]), t

@@ -284,7 +284,50 @@ def gen_singular():
     save("singular", tags=np.array(tags), **store)
 
 
+def gen_backtransform():
+    """rbacktransform / crbacktransform (numba_backend.py:326-375, :759-822) on
+    random rotations, power-of-two segment scales, both modes, a zero column."""
+    rng = np.random.default_rng(21)
+    store = {}
+    tags = []
+    for n, b_r, b, cplx, mode, omega in ((70, 16, 4, False, 1, _DMAX / 2 / 16),
+                                         (70, 16, 4, False, 0, 1e-3),
+                                         (129, 32, 3, True, 1, _DMAX / 2 / 32),
+                                         (129, 32, 3, True, 0, 1e-2),
+                                         (40, 40, 2, False, 0, _DMAX / 2 / 40)):
+        N = (n + b_r - 1) // b_r
+        tile_ends = np.array([min((t + 1) * b_r, n) for t in range(N)], dtype=np.int64)
+        th = rng.uniform(0, 2 * np.pi, (n, b))
+        c = np.cos(th)
+        s = np.sin(th)
+        seg = -rng.integers(0, 300, (N, b)).astype(np.int32)
+        alpha = np.ldexp(1.0, seg)
+        x = rng.standard_normal((n, 2 * b if cplx else b)) * 10.0 ** rng.integers(-5, 5)
+        if b >= 3:
+            x[:, -1] = 0.0  # zero column: no normalisation / sweep (:347-350)
+            if cplx:
+                x[:, -2] = 0.0
+        norms_out = np.zeros(b)
+        alpha_out = np.zeros(b)
+        xo = x.copy()
+        if cplx:
+            phi = rng.uniform(0, 2 * np.pi, (n, b))
+            cre, cim = c * np.cos(phi), c * np.sin(phi)
+            K.crbacktransform(cre, cim, s, alpha, tile_ends, xo, norms_out, alpha_out, mode, omega)
+        else:
+            cre, cim = c, np.zeros_like(c)
+            K.rbacktransform(c, s, alpha, tile_ends, xo, norms_out, alpha_out, mode, omega)
+        t = f"b{len(tags)}"
+        store.update({f"{t}_meta": np.array([n, b_r, b, int(cplx), mode], dtype=np.int64),
+                      f"{t}_omega": np.float64(omega), f"{t}_cre": cre, f"{t}_cim": cim,
+                      f"{t}_s": s, f"{t}_seg": seg, f"{t}_x": x, f"{t}_xout": xo,
+                      f"{t}_norms": norms_out, f"{t}_alpha": alpha_out})
+        tags.append(t)
+    save("backtransform", tags=np.array(tags), **store)
+
+
 if __name__ == "__main__":
+    gen_backtransform()
     gen_singular()
     gen_scalars()
     gen_tiles()
