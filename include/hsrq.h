@@ -15,6 +15,10 @@
  *                      x, per-column alpha, segment scales, represented norms.
  *   hsrq_solve_group_host  the same seam with host (numpy) buffers, as
  *                      _solve_group is called (inviter.py:127-133)
+ *   hsrq_henry_solve   henry_rq_solve, reference.py:21-60 (kernels
+ *                      henry_solve_real / henry_solve_complex,
+ *                      numba_backend.py:830-923): Henry's single-sweep
+ *                      baseline solver, bit-identical to the reference
  *   hsrq_protect_update_batch   protect_update, _kernels/numba_backend.py:47-67
  *   hsrq_hypot_batch            libm hypot as bound by numba (every rotation)
  *   hsrq_tile_diag              reduce_diag + solve_rsolve (numba_backend.py:
@@ -185,6 +189,28 @@ int64_t hsrq_tile_backtransform(int64_t n, int32_t b_r, int32_t b, int32_t cplx,
                                 const double* c_re, const double* c_im, const double* s,
                                 const int32_t* seg_exp, double* x, double* norms,
                                 int32_t* alpha_exp, int32_t mode, double omega, void* stream);
+
+/*
+ * Henry's single-sweep RQ solve (the reference's baseline, henry_rq_solve,
+ * reference.py:21-60): (H - lam_l I) x_l = b_l for m shifts, unguarded, in
+ * one merged factor-and-substitute sweep per shift, followed by the rotation
+ * sweep.  Results are bit-identical to the reference kernels.
+ *   H       n x n column-major (ldh)
+ *   lam     cplx = 0: m doubles; cplx = 1: m (re, im) pairs (complex128)
+ *   X       in: right-hand sides, out: solutions; cplx = 0: n x m doubles,
+ *           column-major (ldx); cplx = 1: n x m complex128 column-major
+ *           (interleaved re, im; ldx counted in complex elements)
+ *   status  optional (may be NULL), per shift: 0 or the packed status
+ *           kind << 42 | shift << 21 | row of that shift's failure
+ *   ws      workspace of >= hsrq_henry_workspace_bytes(n, m, cplx) bytes
+ * Returns, after synchronising `stream`, 0 or the reference's packed status
+ * of the first failure in its loop order (row descending, then shift; kind
+ * HSRQ_KIND_DEGENERATE / HSRQ_KIND_SINGULAR), or a negative HSRQ_ERR_*.
+ */
+size_t hsrq_henry_workspace_bytes(int64_t n, int64_t m, int32_t cplx);
+int64_t hsrq_henry_solve(const double* H, int64_t ldh, int64_t n, const double* lam, int64_t m,
+                         int32_t cplx, double* X, int64_t ldx, int64_t* status, void* ws,
+                         size_t ws_bytes, void* stream);
 
 /* Elementwise device evaluations for bit-level parity of the scalar helpers. */
 int64_t hsrq_protect_update_batch(const double* bnorm, const double* hnorm, const double* xnorm,

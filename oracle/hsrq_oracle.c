@@ -1260,3 +1260,132 @@ int64_t oracle_hsrq_solve(const double* H, int64_t n, int b_r, int b_c, int cplx
     free(btile);
     return st;
 }
+
+/* ------------------------------------------------------------------ */
+/* Henry's single-sweep RQ solve (the reference's baseline solver)      */
+/* ------------------------------------------------------------------ */
+
+/*
+ * oracle_henry_solve_real -- henry_solve_real, K/numba_backend.py:830-873,
+ * behind henry_rq_solve (reference.py:21-60).  H n x n column-major; lam b
+ * shifts; x in/out C-order (n, b).  Loop order kept: kp descending, shifts
+ * inside, so the returned packed status is the reference's first failure.
+ * Ends with the unguarded backtransform (K/numba_backend.py:314-323).
+ */
+int64_t oracle_henry_solve_real(const double* H, int64_t n, int b, const double* lam, double* x) {
+#define HH(i, j) H[(int64_t)(j) * n + (i)]
+    double* v = (double*)malloc(sizeof(double) * (size_t)n * b);
+    double* cc = (double*)malloc(sizeof(double) * (size_t)n * b);
+    double* cs = (double*)malloc(sizeof(double) * (size_t)n * b);
+    int64_t st = 0;
+    for (int64_t i = 0; i < n; i++)
+        for (int l = 0; l < b; l++) v[i * b + l] = HH(i, n - 1);
+    for (int l = 0; l < b; l++) v[(n - 1) * b + l] -= lam[l];
+    for (int l = 0; l < b; l++) {
+        cc[l] = 1.0;
+        cs[l] = 0.0;
+    }
+    for (int64_t kp = n - 1; kp > 0 && !st; kp--) {
+        const double a = HH(kp, kp - 1);
+        for (int l = 0; l < b; l++) {
+            const double vk = v[kp * b + l];
+            const double r = hypot(a, vk);
+            if (r == 0.0) { st = pack_status(KIND_DEGENERATE, l, kp); break; }
+            const double c = vk / r, s = -a / r;
+            cc[kp * b + l] = c;
+            cs[kp * b + l] = s;
+            const double phi = vk * c - a * s;
+            if (phi == 0.0) { st = pack_status(KIND_SINGULAR, l, kp); break; }
+            x[kp * b + l] /= phi;
+            const double tau1 = s * x[kp * b + l], tau2 = c * x[kp * b + l];
+            for (int64_t i = 0; i < kp - 1; i++) {
+                const double hi = HH(i, kp - 1);
+                x[i * b + l] = (x[i * b + l] - tau2 * v[i * b + l]) + tau1 * hi;
+                v[i * b + l] = c * hi + s * v[i * b + l];
+            }
+            const double hd = HH(kp - 1, kp - 1);
+            x[(kp - 1) * b + l] = (x[(kp - 1) * b + l] - tau2 * v[(kp - 1) * b + l]) +
+                                  tau1 * (hd - lam[l]);
+            v[(kp - 1) * b + l] = c * (hd - lam[l]) + s * v[(kp - 1) * b + l];
+        }
+    }
+    if (!st) {
+        for (int l = 0; l < b; l++) {
+            if (v[l] == 0.0) { st = pack_status(KIND_SINGULAR, l, 0); break; }
+            x[l] /= v[l];
+        }
+    }
+    if (!st) oracle_backtransform((int)n, b, cc, cs, x);
+    free(v);
+    free(cc);
+    free(cs);
+    return st;
+}
+
+/*
+ * oracle_henry_solve_complex -- henry_solve_complex, K/numba_backend.py:876-923.
+ * lam: b complex shifts interleaved (re, im); x in/out C-order (n, b) complex
+ * (interleaved doubles, numpy complex128 layout).  numba lowers real*complex
+ * and complex/real by promoting the real to (r, 0).
+ */
+int64_t oracle_henry_solve_complex(const double* H, int64_t n, int b, const double* lam2,
+                                   double* x2) {
+    cplx* v = (cplx*)malloc(sizeof(cplx) * (size_t)n * b);
+    cplx* cc = (cplx*)malloc(sizeof(cplx) * (size_t)n * b);
+    double* cs = (double*)malloc(sizeof(double) * (size_t)n * b);
+    cplx* x = (cplx*)x2;
+    const cplx* lam = (const cplx*)lam2;
+    int64_t st = 0;
+    for (int64_t i = 0; i < n; i++)
+        for (int l = 0; l < b; l++) v[i * b + l] = C(HH(i, n - 1), 0.0);
+    for (int l = 0; l < b; l++) v[(n - 1) * b + l] = csub(v[(n - 1) * b + l], lam[l]);
+    for (int l = 0; l < b; l++) {
+        cc[l] = C(1.0, 0.0);
+        cs[l] = 0.0;
+    }
+    for (int64_t kp = n - 1; kp > 0 && !st; kp--) {
+        const double a = HH(kp, kp - 1);
+        for (int l = 0; l < b; l++) {
+            const cplx vk = v[kp * b + l];
+            const double r = hypot(a, cabs_(vk));
+            if (r == 0.0) { st = pack_status(KIND_DEGENERATE, l, kp); break; }
+            const cplx c = cdiv(vk, C(r, 0.0));
+            const double s = -a / r;
+            cc[kp * b + l] = c;
+            cs[kp * b + l] = s;
+            const cplx cj = C(c.re, -c.im);
+            const cplx phi = csub(cmul(cj, vk), C(a * s, 0.0));
+            if (phi.re == 0.0 && phi.im == 0.0) { st = pack_status(KIND_SINGULAR, l, kp); break; }
+            x[kp * b + l] = cdiv(x[kp * b + l], phi);
+            const cplx tau1 = cmul(C(s, 0.0), x[kp * b + l]);
+            const cplx tau2 = cmul(cj, x[kp * b + l]);
+            for (int64_t i = 0; i < kp - 1; i++) {
+                const cplx hi = C(HH(i, kp - 1), 0.0);
+                x[i * b + l] = cadd(csub(x[i * b + l], cmul(tau2, v[i * b + l])), cmul(tau1, hi));
+                v[i * b + l] = cadd(cmul(c, hi), cmul(C(s, 0.0), v[i * b + l]));
+            }
+            const cplx hdl = csub(C(HH(kp - 1, kp - 1), 0.0), lam[l]);
+            x[(kp - 1) * b + l] =
+                cadd(csub(x[(kp - 1) * b + l], cmul(tau2, v[(kp - 1) * b + l])), cmul(tau1, hdl));
+            v[(kp - 1) * b + l] = cadd(cmul(c, hdl), cmul(C(s, 0.0), v[(kp - 1) * b + l]));
+        }
+    }
+    for (int l = 0; l < b && !st; l++) {
+        if (v[l].re == 0.0 && v[l].im == 0.0) { st = pack_status(KIND_SINGULAR, l, 0); break; }
+        x[l] = cdiv(x[l], v[l]);
+        cplx t1 = x[l];
+        for (int64_t i = 1; i < n; i++) {
+            const cplx t2 = x[i * b + l];
+            const cplx ci = cc[i * b + l];
+            const cplx si = C(cs[i * b + l], 0.0);
+            x[(i - 1) * b + l] = csub(cmul(ci, t1), cmul(si, t2));
+            t1 = cadd(cmul(si, t1), cmul(C(ci.re, -ci.im), t2));
+        }
+        x[(n - 1) * b + l] = t1;
+    }
+    free(v);
+    free(cc);
+    free(cs);
+    return st;
+#undef HH
+}

@@ -247,3 +247,28 @@ def csolve_crsolve(hdiag, hleft, has_left, lam_re, lam_im, rright2, cre, cim, s,
         _p(args[3]), _p(args[4]), _p(args[5]), _p(x2), _p(be, _i32), int(robust),
         ctypes.c_double(omega))
     return st, x2, be
+
+
+def henry_solve(h, lam, b):
+    """Henry's single sweep (henry_solve_real / henry_solve_complex,
+    K/numba_backend.py:830-923) on an (n, m) right-hand side.
+
+    Returns (status, x): the reference's packed status of the first failure
+    (0 = ok) and x (n, m), float64 for real shifts, complex128 for complex."""
+    L = lib()
+    h = np.asfortranarray(h, dtype=np.float64)
+    n = h.shape[0]
+    lam = np.atleast_1d(np.asarray(lam))
+    m = lam.shape[0]
+    if np.iscomplexobj(lam):
+        x = np.ascontiguousarray(np.asarray(b, dtype=np.complex128).reshape(n, m)).copy()
+        lm = np.ascontiguousarray(lam, dtype=np.complex128)
+        f = L.oracle_henry_solve_complex
+    else:
+        x = np.ascontiguousarray(np.asarray(b, dtype=np.float64).reshape(n, m)).copy()
+        lm = np.ascontiguousarray(lam, dtype=np.float64)
+        f = L.oracle_henry_solve_real
+    f.restype = ctypes.c_int64
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    st = int(f(h.ctypes.data, n, m, lm.ctypes.data, x.ctypes.data))
+    return st, x

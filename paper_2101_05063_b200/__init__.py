@@ -27,6 +27,7 @@ from .inviter import (
     starting_vector,
 )
 from .backsolve import chsrq3, dhsrq3
+from .henry import henry_rq_solve
 from . import flops
 
 __version__ = "0.1.0"

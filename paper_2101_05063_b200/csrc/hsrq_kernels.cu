@@ -224,6 +224,8 @@ __global__ void k_zero_bop(double* Bop, int64_t count) {
 
 #include "hsrq_backtransform.cuh"
 
+#include "hsrq_henry.cuh"
+
 // elementwise helpers for parity tests
 __global__ void k_protect_batch(const double* b, const double* h, const double* x, double omega,
                                 int64_t count, double* out) {
@@ -705,6 +707,31 @@ HostLayout host_layout(int64_t n, int b_r, int64_t mc, int64_t mr) {
   L.total = off;
   return L;
 }
+
+// ---------------------------------------------------------------------------
+// Henry's single sweep (hsrq_henry.cuh)
+// ---------------------------------------------------------------------------
+
+struct HenryLayout {
+  size_t v, c, s, st, first, total;
+};
+HenryLayout henry_layout(int64_t n, int64_t m, int cplx) {
+  HenryLayout L;
+  const size_t w = cplx ? 2 : 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = off;
+    off = align_up(off + bytes, 256);
+    return at;
+  };
+  L.v = take(sizeof(double) * w * (size_t)n * m);
+  L.c = take(sizeof(double) * w * (size_t)n * m);
+  L.s = take(sizeof(double) * (size_t)n * m);
+  L.st = take(sizeof(int64_t) * (size_t)m);
+  L.first = take(sizeof(unsigned long long));
+  L.total = off;
+  return L;
+}
 }  // namespace
 
 extern "C" {
@@ -981,6 +1008,64 @@ int64_t hsrq_hypot_batch(const double* x, const double* y, int64_t count, double
   if (count <= 0) return 0;
   k_hypot_batch<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, y, count, out);
   return ck(cudaGetLastError(), "launch") ? 0 : HSRQ_ERR_CUDA;
+}
+
+size_t hsrq_henry_workspace_bytes(int64_t n, int64_t m, int32_t cplx) {
+  return henry_layout(n, m, cplx).total;
+}
+
+int64_t hsrq_henry_solve(const double* H, int64_t ldh, int64_t n, const double* lam, int64_t m,
+                         int32_t cplx, double* X, int64_t ldx, int64_t* status, void* ws,
+                         size_t ws_bytes, void* stream_) {
+  if (n < 1 || m < 1 || ldh < n || ldx < n || n >= (1 << 21) || m >= (1 << 21))
+    return HSRQ_ERR_CONFIG;
+  const HenryLayout L = henry_layout(n, m, cplx);
+  if (ws_bytes < L.total || ws == nullptr) return HSRQ_ERR_WORKSPACE;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  char* w = (char*)ws;
+  HenryArgs a;
+  a.H = H;
+  a.ldh = ldh;
+  a.n = n;
+  a.m = m;
+  a.lam = lam;
+  a.X = X;
+  a.ldx = ldx;
+  a.V = (double*)(w + L.v);
+  a.C = (double*)(w + L.c);
+  a.S = (double*)(w + L.s);
+  a.status = status ? status : (int64_t*)(w + L.st);
+  a.first = (unsigned long long*)(w + L.first);
+  if (!ck(cudaMemsetAsync(a.first, 0, sizeof(unsigned long long), stream), "memset"))
+    return HSRQ_ERR_CUDA;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // threads: whole warps covering n rows, at most HENRY_THREADS
+  const int T = (int)std::min<int64_t>(HENRY_THREADS, ((n + 31) / 32) * 32);
+  // resident CTAs: keep the working set (v, x, c: 3 n-vectors per shift) under
+  // ~half the L2 so the row traffic stays on chip (HSRQ_HENRY_CTAS overrides)
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cplx ? (const void*)k_henry_cplx
+                                                           : (const void*)k_henry_real, T, 0);
+  const double per_shift = 3.0 * 8.0 * (cplx ? 2 : 1) * (double)n;
+  int per_sm = (int)std::max(1.0, std::floor(60.0e6 / (per_shift * sms)));
+  per_sm = std::min(per_sm, std::max(1, occ));
+  if (const char* e = getenv("HSRQ_HENRY_CTAS")) per_sm = std::max(1, atoi(e));
+  const int64_t grid = std::min<int64_t>(m, (int64_t)sms * per_sm);
+  if (cplx)
+    k_henry_cplx<<<(unsigned)grid, T, 0, stream>>>(a);
+  else
+    k_henry_real<<<(unsigned)grid, T, 0, stream>>>(a);
+  int64_t* first = (int64_t*)(w + L.first);  // reuse the key slot for the packed status
+  k_henry_first<<<1, 1, 0, stream>>>(a.first, first);
+  g_launches = 2;
+  int64_t st = 0;
+  if (!ck(cudaGetLastError(), "launch") ||
+      !ck(cudaMemcpyAsync(&st, first, sizeof(int64_t), cudaMemcpyDeviceToHost, stream), "d2h") ||
+      !ck(cudaStreamSynchronize(stream), "sync"))
+    return HSRQ_ERR_CUDA;
+  return st;
 }
 
 }  // extern "C"

@@ -84,3 +84,43 @@ def executed_flops(n, b_r, m_real, m_cplx):
     ncol = m_real + 2 * m_cplx
     N = (n + b_r - 1) // b_r
     return sum(panel_gemm_flops(n, b_r, ncol, jt) for jt in range(1, N))
+
+
+TASK_TYPES = ("ReduceDiag", "ReduceOffdiag", "Solve", "Update", "Backtransform")
+
+
+def _formula(task, dims, cplx):
+    """Leading-order per-shift counts (hessrq flops.py:79-96)."""
+    if task == "ReduceDiag":
+        return (3.0 if cplx else 1.5) * dims[0] ** 2
+    if task == "ReduceOffdiag":
+        return (6.0 if cplx else 3.0) * dims[0] * dims[1]
+    if task == "Solve":
+        return (15.0 if cplx else 3.5) * dims[0] ** 2
+    if task == "Update":
+        return (4.0 if cplx else 2.0) * dims[0] * dims[1]
+    return (20.0 if cplx else 6.0) * (dims[0] - 1)
+
+
+def task_flops(n, b_r, m, cplx):
+    """Per task type: (exact counts, Table-1 formula counts) for m shifts --
+    what the reference's RunStats accumulates over one solve (reduce.py:132,
+    166; backsolve.py:168, 229, 299)."""
+    ranges = [(s, min(s + b_r, n)) for s in range(0, n, b_r)]
+    ex = dict.fromkeys(TASK_TYPES, 0)
+    fo = dict.fromkeys(TASK_TYPES, 0.0)
+    for jt, (js, je) in enumerate(ranges):
+        k = je - js
+        ex["ReduceDiag"] += _reduce_diag(k, cplx)
+        ex["Solve"] += _solve(k, cplx)
+        fo["ReduceDiag"] += _formula("ReduceDiag", (k,), cplx)
+        fo["Solve"] += _formula("Solve", (k,), cplx)
+        for i in range(jt):
+            ki = ranges[i][1] - ranges[i][0]
+            ex["ReduceOffdiag"] += _reduce_offdiag(ki, k, cplx)
+            ex["Update"] += _update(ki, k, cplx)
+            fo["ReduceOffdiag"] += _formula("ReduceOffdiag", (ki, k), cplx)
+            fo["Update"] += _formula("Update", (ki, k), cplx)
+    ex["Backtransform"] += _backtransform(n, cplx)
+    fo["Backtransform"] += _formula("Backtransform", (n,), cplx)
+    return ({t: float(v) * m for t, v in ex.items()}, {t: float(v) * m for t, v in fo.items()})

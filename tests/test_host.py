@@ -77,3 +77,39 @@ def test_shards_balance_flop_cost():
     eigs = np.concatenate([np.arange(5) + 0.5, np.arange(4) + 1j])
     seen = np.concatenate([local_selection(eigs, r, 3)[0] for r in range(3)])
     assert sorted(seen.tolist()) == list(range(9))
+
+
+def test_task_flops_match_reference_runstats():
+    """flops_* / formula_* columns of the bench CSV = the reference's RunStats."""
+    from conftest import golden
+
+    g = golden("runstats")
+    for t in g["tags"]:
+        n, b_r, m, c = (int(v) for v in g[f"{t}_meta"])
+        ex, fo = flops.task_flops(n, b_r, m, bool(c))
+        assert [ex[k] for k in flops.TASK_TYPES] == list(g[f"{t}_flops"])
+        assert [fo[k] for k in flops.TASK_TYPES] == list(g[f"{t}_formula"])
+
+
+def test_bench_csv_inputs_and_header(tmp_path):
+    """Same shifts as the reference bench generator, same leading CSV header,
+    and the reference matrix file format (binary and text) reads back."""
+    import struct
+
+    from conftest import golden
+    from paper_2101_05063_b200 import HessenbergMatrix, benchcsv
+
+    g = golden("runstats")
+    h = HessenbergMatrix(g["shifts_h"])
+    assert np.array_equal(benchcsv.gen_shifts(h, 7, "real"), g["shifts_real"])
+    assert np.array_equal(benchcsv.gen_shifts(h, 7, "complex"), g["shifts_cplx"])
+    ref_head = [str(v) for v in g["bench_header"]]
+    assert benchcsv.header()[: len(ref_head)] == ref_head
+    a = np.asfortranarray(g["shifts_h"])
+    pb = tmp_path / "m.bin"
+    with open(pb, "wb") as f:
+        f.write(b"HSRQ" + struct.pack("<III", 1, a.shape[0], 0) + a.tobytes(order="F"))
+    assert np.array_equal(benchcsv.read_matrix(str(pb)).data, a)
+    pt = tmp_path / "m.txt"
+    pt.write_text(f"{a.shape[0]}\n" + "\n".join(" ".join(repr(float(v)) for v in row) for row in a))
+    assert np.array_equal(benchcsv.read_matrix(str(pt)).data, a)

@@ -103,3 +103,14 @@ def test_singular_shift_reported_like_reference(oracle):
             assert (e.value.shift_index, e.value.local_index) == (shift, row)
             ncase += 1
     assert ncase >= 4
+
+
+def test_henry_bitwise(oracle):
+    """Henry's single sweep: oracle == live reference kernels, bit for bit
+    (status word included; inf/nan positions of the unguarded overflow case)."""
+    g = golden("henry")
+    for t in g["tags"]:
+        st, x = oracle.henry_solve(g[f"{t}_h"], g[f"{t}_lam"], g[f"{t}_b"])
+        assert st == int(g[f"{t}_status"]), t
+        if st == 0:
+            np.testing.assert_array_equal(x, g[f"{t}_x"], err_msg=str(t))

@@ -326,7 +326,133 @@ def gen_backtransform():
     save("backtransform", tags=np.array(tags), **store)
 
 
+def _henry_case(store, tag, h, lam, b):
+    """Henry's kernels as henry_rq_solve (reference.py:21-60) drives them: x and
+    the packed status (0 = ok).  The kernels are called directly because the
+    numba henry_solve_complex falls off its end on success (returns None, not
+    0, K/numba_backend.py:876-923), which makes the public complex wrapper
+    raise TypeError in unpack_status; the real wrapper is checked to agree."""
+    from hessrq.reference import henry_rq_solve
+
+    n = h.shape[0]
+    lam_arr = np.atleast_1d(np.asarray(lam))
+    cplx = np.iscomplexobj(lam_arr)
+    m = lam_arr.shape[0]
+    if cplx:
+        x = np.ascontiguousarray(np.asarray(b, dtype=np.complex128).reshape(n, m)).copy()
+        st = K.henry_solve_complex(np.asfortranarray(h), np.ascontiguousarray(lam_arr, dtype=np.complex128), x)
+    else:
+        x = np.ascontiguousarray(np.asarray(b, dtype=np.float64).reshape(n, m)).copy()
+        st = K.henry_solve_real(np.asfortranarray(h), np.ascontiguousarray(lam_arr, dtype=np.float64), x)
+        if st == 0:
+            xr = henry_rq_solve(h, lam, b)
+            assert np.array_equal(np.asarray(xr).reshape(n, m), x, equal_nan=True)
+    st = 0 if st is None else int(st)
+    store[f"{tag}_h"] = np.asfortranarray(h)
+    store[f"{tag}_lam"] = np.asarray(lam)
+    store[f"{tag}_b"] = np.asarray(b)
+    store[f"{tag}_status"] = np.int64(st)
+    if st == 0:
+        store[f"{tag}_x"] = x
+
+
+def gen_henry():
+    """Henry's single sweep (K/numba_backend.py:830-923 via reference.py:21-60):
+    random shifts, eigenvalue shifts (near-singular), n = 1/2, a scalar shift
+    with a 1-D rhs, an overflowing rhs (unguarded: inf/nan propagate), an
+    exactly singular integer system and a degenerate (zero subdiagonal) one."""
+    rng = np.random.default_rng(41)
+    store = {}
+    tags = []
+
+    def add(h, lam, b):
+        t = f"y{len(tags)}"
+        _henry_case(store, t, h, lam, b)
+        tags.append(t)
+
+    for n, m, seed in ((1, 2, 1), (2, 3, 2), (5, 3, 3), (40, 4, 4), (129, 5, 5), (300, 3, 6)):
+        h = np.array(random_unreduced(n, seed).data)
+        nrm = np.max(np.sum(np.abs(h), axis=1))
+        add(h, nrm * rng.uniform(-2, 2, m), rng.standard_normal((n, m)))
+        add(h, nrm * (rng.uniform(-2, 2, m) + 1j * rng.uniform(0.05, 2, m)),
+            rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m)))
+        if n >= 5:
+            ev = np.linalg.eigvals(h)
+            er, ec = ev[ev.imag == 0].real[:3], ev[ev.imag > 0][:3]
+            if er.size:
+                add(h, er, np.ones((n, er.size)))
+            if ec.size:
+                add(h, ec, np.ones((n, ec.size)) + 0j)
+    h = np.array(random_unreduced(30, 9).data)
+    add(h, 0.75, rng.standard_normal(30))                       # scalar shift, 1-D rhs
+    add(h, 0.75 + 0.5j, rng.standard_normal(30) + 0j)
+    add(np.array(gen_h2(60).data), np.array([2.0]), 1e290 * np.ones((60, 1)))
+    add(np.array(gen_h2(60).data), np.array([2.0 + 0.5j]), 1e290 * np.ones((60, 1)) + 0j)
+    # exactly singular: small-integer H with an integer eigenvalue
+    for trial in range(5000):
+        hi = np.triu(rng.integers(-2, 3, (8, 8))).astype(float)
+        hi[np.arange(1, 8), np.arange(7)] = rng.choice([-2.0, -1.0, 1.0, 2.0], 7)
+        ev = np.linalg.eigvals(hi)
+        ints = [round(e.real) for e in ev if abs(e.imag) < 1e-12 and abs(e.real - round(e.real)) < 1e-12]
+        if ints:
+            lam = np.array([ints[0] + 0.25, float(ints[0]), ints[0] + 0.5])
+            add(hi, lam, np.ones((8, 3)))
+            add(hi, lam + 0j, np.ones((8, 3)) + 0j)
+            break
+    # singular final pivot: v[0] = c(h00 - lam) + s h01 cancels exactly (c = -s)
+    h2 = np.array([[2.0, 1.0], [1.0, 2.0]])
+    add(h2, np.array([0.5, 1.0, 3.0]), np.ones((2, 3)))
+    add(h2, np.array([0.5 + 0.5j, 1.0 + 0j, 3.0 + 0j]), np.ones((2, 3)) + 0j)
+    # degenerate rotation: a = h[n-1, n-2] = 0 and v[n-1] = h[n-1, n-1] - lam = 0
+    hd = np.triu(rng.standard_normal((6, 6)), -1)
+    hd[5, 4] = 0.0
+    add(hd, np.array([0.3, hd[5, 5]]), np.ones((6, 2)))
+    add(hd, np.array([0.3 + 0.1j, hd[5, 5] + 0j]), np.ones((6, 2)) + 0j)
+    save("henry", tags=np.array(tags), **store)
+
+
+def gen_runstats():
+    """RunStats flops / formula per task type of reference solves (the bench
+    CSV's flops_* and formula_* columns, cli.py:320-364)."""
+    from hessrq.scheduler import RunStats
+
+    store = {}
+    tags = []
+    for n, b_r, m, cplx in ((300, 64, 3, False), (300, 64, 3, True), (129, 32, 2, True),
+                            (200, 200, 2, False)):
+        h = random_unreduced(n, 3)
+        lam = np.linspace(0.5, 1.5, m) * h.infinity_norm() * 2 + (0.3j if cplx else 0)
+        b = np.ones((n, m), dtype=complex if cplx else float)
+        st = RunStats()
+        (chsrq3 if cplx else dhsrq3)(h, lam, b, b_r=b_r, b_c=8, stats=st)
+        t = f"r{len(tags)}"
+        store[f"{t}_meta"] = np.array([n, b_r, m, int(cplx)], dtype=np.int64)
+        store[f"{t}_flops"] = np.array([st.flops.get(k, 0.0) for k in
+                                        ("ReduceDiag", "ReduceOffdiag", "Solve", "Update", "Backtransform")])
+        store[f"{t}_formula"] = np.array([st.formula.get(k, 0.0) for k in
+                                          ("ReduceDiag", "ReduceOffdiag", "Solve", "Update", "Backtransform")])
+        tags.append(t)
+    # the bench command's shift generator and CSV header (cli.py:79-95, 320-331)
+    from hessrq import cli
+
+    hb = random_unreduced(50, 4)
+    store["shifts_real"] = cli.load_shifts("gen:count=7,kind=real,seed=2,radius=1.5", hb)
+    store["shifts_cplx"] = cli.load_shifts("gen:count=7,kind=complex,seed=2,radius=1.5", hb)
+    store["shifts_h"] = np.asfortranarray(hb.data)
+    store["bench_header"] = np.array(
+        ["schema", "backend", "n", "m", "kind", "b_r", "b_c", "workers", "robust"]
+        + list(cli.TASK_TYPES) + ["total_s"] + [f"flops_{t}" for t in cli.TASK_TYPES]
+        + [f"formula_{t}" for t in cli.TASK_TYPES] + ["henry_s"])
+    save("runstats", tags=np.array(tags), **store)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate selected fixtures: make_golden.py henry tiles ...
+        for name in sys.argv[1:]:
+            globals()[f"gen_{name}"]()
+        sys.exit(0)
+    gen_runstats()
+    gen_henry()
     gen_backtransform()
     gen_singular()
     gen_scalars()
