@@ -19,6 +19,9 @@
  *                      henry_solve_real / henry_solve_complex,
  *                      numba_backend.py:830-923): Henry's single-sweep
  *                      baseline solver, bit-identical to the reference
+ *   hsrq_compact_encode / hsrq_compact_decode
+ *                      GivensTable.compact / from_compact (core.py:193-209,
+ *                      givens.py:90-198): Stewart's compact rotation codes
  *   hsrq_protect_update_batch   protect_update, _kernels/numba_backend.py:47-67
  *   hsrq_hypot_batch            libm hypot as bound by numba (every rotation)
  *   hsrq_tile_diag              reduce_diag + solve_rsolve (numba_backend.py:
@@ -57,6 +60,14 @@ extern "C" {
 #define HSRQ_KIND_DEGENERATE 1 /* numba_backend.py:17 */
 #define HSRQ_KIND_SINGULAR 2   /* numba_backend.py:18 */
 
+/* Flag or-ed into `mode` of the solve entry points: store the recorded
+ * rotations in Stewart's compact form (GivensTable.compact(), core.py:193-209,
+ * givens.py:90-198) -- c_re holds the code t of a real shift / t1 of a
+ * complex shift, c_im holds t2 of complex shift q < m_cplx (row q), s is
+ * not used (may be NULL): 2 instead of 3 reals per complex rotation, 1
+ * instead of 2 per real one.  The backtransform decodes the codes. */
+#define HSRQ_MODE_COMPACT_ROTATIONS 0x10
+
 /* Error codes (negative returns). */
 #define HSRQ_ERR_CONFIG (-1)   /* b_r outside [1, 128], n < 1, bad sizes */
 #define HSRQ_ERR_WORKSPACE (-2) /* workspace too small */
@@ -92,7 +103,8 @@ size_t hsrq_workspace_bytes(int64_t n, int32_t b_r, int64_t m_cplx, int64_t m_re
  *  fail     out, per shift: 0, or (phase << 56) | (tile << 24) | row of the
  *           first failure (phase 1 = degenerate rotation, 2 = singular factor)
  *  robust   1 = robust_tiled_solve (Omega = DBL_MAX/2/b_r), 0 = tiled_solve
- *  mode     1 = eigvec (normalise), 0 = solve
+ *  mode     1 = eigvec (normalise), 0 = solve; | HSRQ_MODE_COMPACT_ROTATIONS
+ *           for compact rotation storage
  *  ws       workspace of >= hsrq_workspace_bytes(...) bytes
  *
  * Returns the number of failed shifts (>= 0) after synchronising `stream`,
@@ -211,6 +223,18 @@ size_t hsrq_henry_workspace_bytes(int64_t n, int64_t m, int32_t cplx);
 int64_t hsrq_henry_solve(const double* H, int64_t ldh, int64_t n, const double* lam, int64_t m,
                          int32_t cplx, double* X, int64_t ldx, int64_t* status, void* ws,
                          size_t ws_bytes, void* stream);
+
+/*
+ * Stewart compact rotation codes, elementwise over `count` rotations
+ * (compact_encode / compact_decode and the complex pair, givens.py:107-198;
+ * GivensTable.compact / from_compact, core.py:193-209), bit-identical to the
+ * reference.  Real (cplx = 0): (c_re, s) <-> t1 (c_im, t2 unused).  Complex:
+ * (c_re, c_im, s) <-> (t1, t2).
+ */
+int64_t hsrq_compact_encode(int64_t count, int32_t cplx, const double* c_re, const double* c_im,
+                            const double* s, double* t1, double* t2, void* stream);
+int64_t hsrq_compact_decode(int64_t count, int32_t cplx, const double* t1, const double* t2,
+                            double* c_re, double* c_im, double* s, void* stream);
 
 /* Elementwise device evaluations for bit-level parity of the scalar helpers. */
 int64_t hsrq_protect_update_batch(const double* bnorm, const double* hnorm, const double* xnorm,

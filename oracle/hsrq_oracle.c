@@ -1389,3 +1389,64 @@ int64_t oracle_henry_solve_complex(const double* H, int64_t n, int b, const doub
     return st;
 #undef HH
 }
+
+/* ------------------------------------------------------------------ */
+/* Stewart compact rotation codes, givens.py:90-198                    */
+/* ------------------------------------------------------------------ */
+
+static double compact_encode1(double c, double s) { /* compact_encode, givens.py:107-113 */
+    if (fabs(s) <= fabs(c)) {
+        const double base = c >= 0.0 ? 0.0 : 2.0;
+        return s != 0.0 ? copysign(fabs(s) + base, s) : base;
+    }
+    const double base = s >= 0.0 ? 4.0 : 6.0;
+    return c != 0.0 ? copysign(fabs(c) + base, c) : base;
+}
+
+static double max0(double u) { return u > 0.0 ? u : 0.0; } /* Python max(0.0, u) */
+
+static void compact_decode1(double t, double* c, double* s) { /* givens.py:116-131 */
+    const double at = fabs(t);
+    if (at <= 1.0) {
+        *s = t;
+        *c = sqrt(max0(1.0 - *s * *s));
+    } else if (at <= 3.0) {
+        *s = at != 2.0 ? copysign(at - 2.0, t) : 0.0;
+        *c = -sqrt(max0(1.0 - *s * *s));
+    } else if (at <= 5.0) {
+        *c = at != 4.0 ? copysign(at - 4.0, t) : 0.0;
+        *s = sqrt(max0(1.0 - *c * *c));
+    } else {
+        *c = at != 6.0 ? copysign(at - 6.0, t) : 0.0;
+        *s = -sqrt(max0(1.0 - *c * *c));
+    }
+}
+
+/* compact_encode_table(_complex) / compact_decode_table(_complex), elementwise. */
+void oracle_compact_encode(int64_t count, int cplx, const double* c_re, const double* c_im,
+                           const double* s, double* t1, double* t2) {
+    for (int64_t i = 0; i < count; i++) {
+        if (!cplx) {
+            t1[i] = compact_encode1(c_re[i], s[i]);
+            continue;
+        }
+        const double ac = hypot(c_re[i], c_im[i]); /* abs(complex) */
+        t1[i] = compact_encode1(ac, s[i]);
+        t2[i] = ac == 0.0 ? compact_encode1(1.0, 0.0) : compact_encode1(c_re[i] / ac, c_im[i] / ac);
+    }
+}
+
+void oracle_compact_decode(int64_t count, int cplx, const double* t1, const double* t2,
+                           double* c_re, double* c_im, double* s) {
+    for (int64_t i = 0; i < count; i++) {
+        if (!cplx) {
+            compact_decode1(t1[i], &c_re[i], &s[i]);
+            continue;
+        }
+        double ac, dc, ds;
+        compact_decode1(t1[i], &ac, &s[i]);
+        compact_decode1(t2[i], &dc, &ds);
+        c_re[i] = ac * dc;
+        c_im[i] = ac * ds;
+    }
+}

@@ -272,3 +272,34 @@ def henry_solve(h, lam, b):
     f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
     st = int(f(h.ctypes.data, n, m, lm.ctypes.data, x.ctypes.data))
     return st, x
+
+
+def compact_encode(c_re, s, c_im=None):
+    """givens.compact_encode_table / _complex: t (real) or (t1, t2) (complex)."""
+    L = lib()
+    c_re = np.ascontiguousarray(c_re, dtype=np.float64)
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    t1 = np.empty_like(c_re)
+    L.oracle_compact_encode.restype = None
+    if c_im is None:
+        L.oracle_compact_encode(ctypes.c_int64(c_re.size), 0, _p(c_re), None, _p(s), _p(t1), None)
+        return t1
+    c_im = np.ascontiguousarray(c_im, dtype=np.float64)
+    t2 = np.empty_like(c_re)
+    L.oracle_compact_encode(ctypes.c_int64(c_re.size), 1, _p(c_re), _p(c_im), _p(s), _p(t1), _p(t2))
+    return t1, t2
+
+
+def compact_decode(t1, t2=None):
+    """givens.compact_decode_table / _complex: (c, s) or (c_re, c_im, s)."""
+    L = lib()
+    t1 = np.ascontiguousarray(t1, dtype=np.float64)
+    c, s = np.empty_like(t1), np.empty_like(t1)
+    L.oracle_compact_decode.restype = None
+    if t2 is None:
+        L.oracle_compact_decode(ctypes.c_int64(t1.size), 0, _p(t1), None, _p(c), None, _p(s))
+        return c, s
+    t2 = np.ascontiguousarray(t2, dtype=np.float64)
+    ci = np.empty_like(t1)
+    L.oracle_compact_decode(ctypes.c_int64(t1.size), 1, _p(t1), _p(t2), _p(c), _p(ci), _p(s))
+    return c, ci, s

@@ -52,6 +52,8 @@ SIGNATURES = {
     "hsrq_protect_update_batch": (_i64, [_p, _p, _p, _f64, _i64, _p, _p]),
     "hsrq_hypot_batch": (_i64, [_p, _p, _i64, _p, _p]),
     "hsrq_debug_counters": (_i64, [_p, _i32]),
+    "hsrq_compact_encode": (_i64, [_i64, _i32, _p, _p, _p, _p, _p, _p]),
+    "hsrq_compact_decode": (_i64, [_i64, _i32, _p, _p, _p, _p, _p, _p]),
     "hsrq_henry_workspace_bytes": (_sz, [_i64, _i64, _i32]),
     "hsrq_henry_solve": (_i64, [_p, _i64, _i64, _p, _i64, _i32, _p, _i64, _p, _p, _sz, _p]),
 }

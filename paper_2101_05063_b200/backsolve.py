@@ -14,7 +14,7 @@ from .solver import MAX_TILE, raise_first_failure, solve_group, to_solution_bloc
 
 
 def _driver(h, shifts, b, kind, *, b_r=None, b_c=32, workers=1, robust=True, mode="solve",
-            stats=None, budget=None, workspace=None, device=None):
+            stats=None, budget=None, workspace=None, device=None, compact_rotations=False):
     h = as_hessenberg(h)
     if not h.is_unreduced():
         raise ConfigError("matrix must be unreduced (nonzero subdiagonal)")
@@ -29,13 +29,13 @@ def _driver(h, shifts, b, kind, *, b_r=None, b_c=32, workers=1, robust=True, mod
         B[0::2] = bb.real.T
         B[1::2] = bb.imag.T
         out, _ = solve_group(h, lam, None, B, b_r, robust=robust, mode=mode, b_c=b_c,
-                             device=device)
+                             device=device, compact=compact_rotations)
     else:
         lam = np.asarray(shifts, dtype=np.float64).ravel()
         m = lam.size
         B = np.ascontiguousarray(np.asarray(b, dtype=np.float64).reshape(n, m).T)
         out, _ = solve_group(h, None, lam, B, b_r, robust=robust, mode=mode, b_c=b_c,
-                             device=device)
+                             device=device, compact=compact_rotations)
     if out.nfail:
         raise_first_failure(out.fail.cpu().numpy(), b_c, [(0, m)])
     return to_solution_block(out, n, robust=robust, want_cplx=(kind == "complex"))

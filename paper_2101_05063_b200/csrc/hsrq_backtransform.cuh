@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(BT_WARPS * 32) k_backtransform(Ctx c, int32_t*
   double* xi = cplx ? c.X + (col + 1) * c.ldx : nullptr;
   const double* cr = c.c_re + q * c.ldc;
   const double* ci = cplx ? c.c_im + q * c.ldc : nullptr;
-  const double* ss = c.s + q * c.ldc;
+  const double* ss = c.compact ? nullptr : c.s + q * c.ldc;
   const double qnan = __longlong_as_double(0x7ff8000000000000LL);
   if (c.fail[q] != 0) {
     if (lane == 0) {
@@ -133,9 +133,16 @@ __global__ void __launch_bounds__(BT_WARPS * 32) k_backtransform(Ctx c, int32_t*
         a *= sc;
         if (cplx) b *= sc;
       }
-      cc = cr[i];
-      sv = ss[i];
-      if (cplx) cim = ci[i];
+      if (c.compact) {  // Stewart codes (givens.py:107-124, :144-149)
+        if (cplx)
+          compact_decode_cplx(cr[i], ci[i], cc, cim, sv);
+        else
+          compact_decode(cr[i], cc, sv);
+      } else {
+        cc = cr[i];
+        sv = ss[i];
+        if (cplx) cim = ci[i];
+      }
     }
     const int cnt = (int)(n - base < 32 ? n - base : 32);
     double outr = 0.0, outi = 0.0;

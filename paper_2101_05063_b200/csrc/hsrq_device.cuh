@@ -161,4 +161,57 @@ __device__ __forceinline__ unsigned long long dkey(double v) {
 }
 __device__ __forceinline__ double dval(unsigned long long k) { return __longlong_as_double((long long)k); }
 
+
+// ---------------------------------------------------------------------------
+// Stewart compact rotation storage (givens.py:90-198): one real per real
+// rotation, two per complex rotation.  The smaller component is stored, the
+// window offset (0/2/4/6) records which one and the sign of the other.
+// Expression for expression the reference's, so encode and decode are
+// bit-identical to compact_encode / compact_decode (IEEE add/sqrt/div).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double compact_encode(double c, double s) {
+  if (fabs(s) <= fabs(c)) {
+    const double base = c >= 0.0 ? 0.0 : 2.0;
+    return s != 0.0 ? copysign(fabs(s) + base, s) : base;
+  }
+  const double base = s >= 0.0 ? 4.0 : 6.0;
+  return c != 0.0 ? copysign(fabs(c) + base, c) : base;
+}
+
+__device__ __forceinline__ double pmax0(double u) { return u > 0.0 ? u : 0.0; }  // max(0.0, u)
+
+__device__ __forceinline__ void compact_decode(double t, double& c, double& s) {
+  const double at = fabs(t);
+  if (at <= 1.0) {
+    s = t;
+    c = __dsqrt_rn(pmax0(1.0 - s * s));
+  } else if (at <= 3.0) {
+    s = at != 2.0 ? copysign(at - 2.0, t) : 0.0;
+    c = -__dsqrt_rn(pmax0(1.0 - s * s));
+  } else if (at <= 5.0) {
+    c = at != 4.0 ? copysign(at - 4.0, t) : 0.0;
+    s = __dsqrt_rn(pmax0(1.0 - c * c));
+  } else {
+    c = at != 6.0 ? copysign(at - 6.0, t) : 0.0;
+    s = -__dsqrt_rn(pmax0(1.0 - c * c));
+  }
+}
+
+// compact_encode_complex: (|c|, s) and the unit direction of c.
+__device__ __forceinline__ void compact_encode_cplx(double cr, double ci, double s, double& t1,
+                                                    double& t2) {
+  const double ac = ghypot(cr, ci);
+  t1 = compact_encode(ac, s);
+  t2 = ac == 0.0 ? compact_encode(1.0, 0.0) : compact_encode(cr / ac, ci / ac);
+}
+
+__device__ __forceinline__ void compact_decode_cplx(double t1, double t2, double& cr, double& ci,
+                                                    double& s) {
+  double ac, dc, ds;
+  compact_decode(t1, ac, s);
+  compact_decode(t2, dc, ds);
+  cr = ac * dc;
+  ci = ac * ds;
+}
+
 }  // namespace hsrq

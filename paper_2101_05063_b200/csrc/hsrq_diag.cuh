@@ -44,6 +44,8 @@ struct DiagArgs {
   int k;
   int has_left;
   int64_t q0, count;  // shifts [q0, q0 + count) handled by this launch
+  int64_t rot_off;    // row offset of this tile in the rotation table (js; 0 when the
+                      // diag launch records into the compact mode's tile scratch)
   // tile-level mode (hsrq_tile_diag): explicit buffers, shifts 0..t_b-1
   int tile_mode;
   const double* t_hdiag;   // k x (k-1) row-major
@@ -120,9 +122,9 @@ __device__ __forceinline__ void put_rot(const Ctx& c, const DiagArgs& a, int64_t
     if (a.t_cim) a.t_cim[(int64_t)row * a.t_b + q] = ci;
     a.t_s[(int64_t)row * a.t_b + q] = s;
   } else {
-    c.c_re[q * c.ldc + a.js + row] = cr;
-    if (c.c_im) c.c_im[q * c.ldc + a.js + row] = ci;
-    c.s[q * c.ldc + a.js + row] = s;
+    c.c_re[q * c.ldc + a.rot_off + row] = cr;
+    if (c.c_im) c.c_im[q * c.ldc + a.rot_off + row] = ci;
+    c.s[q * c.ldc + a.rot_off + row] = s;
   }
 }
 
@@ -301,8 +303,8 @@ __global__ void __launch_bounds__(DW * 32) k_diag_real(Ctx c, DiagArgs a) {
   // ---- panel operands: W_j = c_j prod_{t<j} s_t, P; Z (update_rupdate :246-253) ----
   double* bw = c.Bop + (2 * col) * KP;
   double* bz = c.Bop + (2 * col + 1) * KP;
-  const double* crow = c.c_re + (live ? q : 0) * c.ldc + a.js;
-  const double* srow = c.s + (live ? q : 0) * c.ldc + a.js;
+  const double* crow = c.c_re + (live ? q : 0) * c.ldc + a.rot_off;
+  const double* srow = c.s + (live ? q : 0) * c.ldc + a.rot_off;
   double pre = 1.0;
   double carry = c0 * x0;  // Z[0] = c[0] * Z[0]
   for (int j = 0; j < k; j++) {
@@ -644,9 +646,9 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
   double* bw_im = c.Bop + (2 * (col + 1)) * KP;
   double* bz_im = c.Bop + (2 * (col + 1) + 1) * KP;
   const int64_t qs = live ? q : 0;
-  const double* crow = c.c_re + qs * c.ldc + a.js;
-  const double* cirow = c.c_im + qs * c.ldc + a.js;
-  const double* srow = c.s + qs * c.ldc + a.js;
+  const double* crow = c.c_re + qs * c.ldc + a.rot_off;
+  const double* cirow = c.c_im + qs * c.ldc + a.rot_off;
+  const double* srow = c.s + qs * c.ldc + a.rot_off;
   double pre = 1.0;
   cplx carry = mk(c0r * x0.re + c0i * x0.im, c0r * x0.im - c0i * x0.re);
   for (int j = 0; j < k; j++) {

@@ -85,6 +85,11 @@ struct Ctx {
   double* Cr;            // crossover, n x ncol (ld ldx)
   double *c_re, *c_im, *s;
   int64_t ldc;
+  int compact;           // HSRQ_MODE_COMPACT_ROTATIONS: c_re holds the Stewart code t
+                         // (real) / t1 (complex), c_im holds t2 of complex shift q < mc,
+                         // s is unused (givens.py:90-198)
+  double* Rt;            // compact mode: exact rotations of the current tile column,
+                         // [c_re | c_im | s] x ms x KP (the panel operands need them)
   int32_t* E;            // N x ms
   double* Bop;           // (2*ncol_pad) x KP
   StepScalars* SS;       // ms
@@ -235,6 +240,44 @@ __global__ void k_protect_batch(const double* b, const double* h, const double* 
     out[t] = p2(e);
   }
 }
+__global__ void k_compact_encode(int64_t count, int cplx, const double* c_re, const double* c_im,
+                                 const double* s, double* t1, double* t2) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  if (cplx)
+    compact_encode_cplx(c_re[t], c_im[t], s[t], t1[t], t2[t]);
+  else
+    t1[t] = compact_encode(c_re[t], s[t]);
+}
+
+__global__ void k_compact_decode(int64_t count, int cplx, const double* t1, const double* t2,
+                                 double* c_re, double* c_im, double* s) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  if (cplx)
+    compact_decode_cplx(t1[t], t2[t], c_re[t], c_im[t], s[t]);
+  else
+    compact_decode(t1[t], c_re[t], s[t]);
+}
+
+// Compact mode: Stewart codes of tile rows [js, js + k) from the tile scratch
+// (one thread per (row, shift); failed shifts' rows are encoded too, harmless).
+__global__ void k_compact_tile(Ctx c, int64_t js, int k) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)k * c.ms) return;
+  const int64_t q = t / k;
+  const int row = (int)(t - q * k);
+  const double cr = c.Rt[q * KP + row], s = c.Rt[(2 * c.ms + q) * KP + row];
+  if (q < c.mc) {
+    double t1, t2;
+    compact_encode_cplx(cr, c.Rt[(c.ms + q) * KP + row], s, t1, t2);
+    c.c_re[q * c.ldc + js + row] = t1;
+    c.c_im[q * c.ldc + js + row] = t2;
+  } else {
+    c.c_re[q * c.ldc + js + row] = compact_encode(cr, s);
+  }
+}
+
 __global__ void k_hypot_batch(const double* x, const double* y, int64_t count, double* out) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t < count) out[t] = ghypot(x[t], y[t]);
@@ -336,7 +379,7 @@ void diag_launch(bool cplx, const Ctx& c, const DiagArgs& a, cudaStream_t s) {
 }
 
 struct WsLayout {
-  size_t cr, bop, ss, hm0, rs, hmk, xb, rsc, nfail, total;
+  size_t cr, bop, ss, hm0, rs, hmk, xb, rsc, rt, nfail, total;
 };
 
 WsLayout ws_layout(int64_t n, int b_r, int64_t mc, int64_t mr) {
@@ -364,6 +407,8 @@ WsLayout ws_layout(int64_t n, int b_r, int64_t mc, int64_t mr) {
   off = align_up(off + sizeof(double) * (size_t)N * ms, 256);
   L.rsc = off;
   off = align_up(off + 64 * (size_t)N * ms, 256);
+  L.rt = off;
+  off = align_up(off + sizeof(double) * 3 * (size_t)KP * ms, 256);
   L.total = off;
   return L;
 }
@@ -427,7 +472,9 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   c.fail = fail;
   c.nfail = (unsigned long long*)(w + L.nfail);
   c.robust = robust;
-  c.mode = mode;
+  c.mode = mode & 1;
+  c.compact = (mode & HSRQ_MODE_COMPACT_ROTATIONS) ? 1 : 0;
+  c.Rt = (double*)(w + L.rt);
   c.diag_gemm_only = getenv("HSRQ_PANEL_GEMM_ONLY") ? atoi(getenv("HSRQ_PANEL_GEMM_ONLY")) : 0;
   c.diag_tl = nullptr;
   c.diag_tl_jt = -1;
@@ -559,21 +606,38 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
       cudaEventRecord(ev_fork, stream);
       cudaStreamWaitEvent(side, ev_fork, 0);
     }
+    // Compact rotation storage: the diagonal kernels record the tile's exact
+    // rotations into the tile scratch Rt (the panel operands need them), and
+    // k_compact_tile writes their Stewart codes into the tables.
+    Ctx cd = c;
+    a.rot_off = a.js;
+    if (c.compact) {
+      cd.c_re = c.Rt;
+      cd.c_im = c.Rt + c.ms * KP;
+      cd.s = c.Rt + 2 * c.ms * KP;
+      cd.ldc = KP;
+      a.rot_off = 0;
+    }
     if (mr > 0) {
       a.q0 = mc;
       a.count = mr;
-      diag_launch(false, c, a, fork ? side : stream);
+      diag_launch(false, cd, a, fork ? side : stream);
       g_launches++;
     }
     if (mc > 0) {
       a.q0 = 0;
       a.count = mc;
-      diag_launch(true, c, a, stream);
+      diag_launch(true, cd, a, stream);
       g_launches++;
     }
     if (fork) {
       cudaEventRecord(ev_join, side);
       cudaStreamWaitEvent(stream, ev_join, 0);
+    }
+    if (c.compact) {
+      const int64_t cnt = (int64_t)a.k * c.ms;
+      k_compact_tile<<<(unsigned)((cnt + 255) / 256), 256, 0, stream>>>(c, a.js, a.k);
+      g_launches++;
     }
     if (g_timing) cudaEventRecord(ev[2 + 3 * jt], stream);
     if (jt > 0) {
@@ -1066,6 +1130,22 @@ int64_t hsrq_henry_solve(const double* H, int64_t ldh, int64_t n, const double* 
       !ck(cudaStreamSynchronize(stream), "sync"))
     return HSRQ_ERR_CUDA;
   return st;
+}
+
+int64_t hsrq_compact_encode(int64_t count, int32_t cplx, const double* c_re, const double* c_im,
+                            const double* s, double* t1, double* t2, void* stream) {
+  if (count <= 0) return 0;
+  k_compact_encode<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      count, cplx, c_re, c_im, s, t1, t2);
+  return ck(cudaGetLastError(), "launch") ? 0 : HSRQ_ERR_CUDA;
+}
+
+int64_t hsrq_compact_decode(int64_t count, int32_t cplx, const double* t1, const double* t2,
+                            double* c_re, double* c_im, double* s, void* stream) {
+  if (count <= 0) return 0;
+  k_compact_decode<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      count, cplx, t1, t2, c_re, c_im, s);
+  return ck(cudaGetLastError(), "launch") ? 0 : HSRQ_ERR_CUDA;
 }
 
 }  // extern "C"

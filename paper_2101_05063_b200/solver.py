@@ -72,9 +72,9 @@ class GroupOutput:
     """Device-side results of one solve group (torch tensors)."""
 
     X: torch.Tensor          # (ncol, n): row c = column c
-    c_re: torch.Tensor       # (ms, n)
-    c_im: torch.Tensor
-    s: torch.Tensor
+    c_re: torch.Tensor       # (ms, n); compact: Stewart code t (real) / t1 (complex)
+    c_im: torch.Tensor       # (ms, n); compact: (mc, n) codes t2
+    s: torch.Tensor          # (ms, n); compact: None
     seg_exp: torch.Tensor    # (N, ms) int32
     alpha_exp: torch.Tensor  # (ms,) int32
     norms: torch.Tensor
@@ -84,12 +84,67 @@ class GroupOutput:
     mc: int
     mr: int
     launches: int
+    compact: bool = False
+
+    def rotations(self):
+        """The recorded rotations as (c_re, c_im, s) device tensors (ms, n),
+        decoded from the compact codes when stored compactly (hsrq_compact_decode)."""
+        if not self.compact:
+            return self.c_re, self.c_im, self.s
+        lib = _lib.load()
+        ms, n = self.c_re.shape
+        cr, ci, s = (torch.zeros((ms, n), dtype=torch.float64, device=self.c_re.device)
+                     for _ in range(3))
+        st = ctypes.c_void_p(torch.cuda.current_stream(self.c_re.device).cuda_stream)
+        if self.mc:
+            lib.hsrq_compact_decode(self.mc * n, 1, _ptr(self.c_re), _ptr(self.c_im), _ptr(cr),
+                                    _ptr(ci), _ptr(s), st)
+        if self.mr:
+            off = self.mc
+            lib.hsrq_compact_decode(self.mr * n, 0, _ptr(self.c_re[off:]), None, _ptr(cr[off:]),
+                                    None, _ptr(s[off:]), st)
+        return cr, ci, s
+
+
+def compact_encode(c_re, c_im, s):
+    """GivensTable.compact() on device tensors (core.py:193-199): real tables
+    (c_im None) -> t; complex -> (t1, t2).  Bit-identical to givens.py."""
+    lib = _lib.load()
+    st = ctypes.c_void_p(torch.cuda.current_stream(c_re.device).cuda_stream)
+    c_re, s = c_re.contiguous(), s.contiguous()
+    t1 = torch.empty_like(c_re)
+    if c_im is None:
+        lib.hsrq_compact_encode(c_re.numel(), 0, _ptr(c_re), None, _ptr(s), _ptr(t1), None, st)
+        return t1
+    c_im = c_im.contiguous()
+    t2 = torch.empty_like(c_re)
+    lib.hsrq_compact_encode(c_re.numel(), 1, _ptr(c_re), _ptr(c_im), _ptr(s), _ptr(t1), _ptr(t2), st)
+    return t1, t2
+
+
+def compact_decode(t1, t2=None):
+    """GivensTable.from_compact() on device tensors (core.py:201-209):
+    returns (c, s) for real codes, (c_re, c_im, s) for complex pairs."""
+    lib = _lib.load()
+    st = ctypes.c_void_p(torch.cuda.current_stream(t1.device).cuda_stream)
+    t1 = t1.contiguous()
+    c, s = torch.empty_like(t1), torch.empty_like(t1)
+    if t2 is None:
+        lib.hsrq_compact_decode(t1.numel(), 0, _ptr(t1), None, _ptr(c), None, _ptr(s), st)
+        return c, s
+    t2 = t2.contiguous()
+    ci = torch.empty_like(t1)
+    lib.hsrq_compact_decode(t1.numel(), 1, _ptr(t1), _ptr(t2), _ptr(c), _ptr(ci), _ptr(s), st)
+    return c, ci, s
+
+
+MODE_COMPACT_ROTATIONS = 0x10  # include/hsrq.h
 
 
 class GroupSolver:
     """Device buffers for one (n, b_r, m_cplx, m_real) shape, reusable across calls."""
 
-    def __init__(self, dh: DeviceHessenberg, b_r, m_cplx, m_real):
+    def __init__(self, dh: DeviceHessenberg, b_r, m_cplx, m_real, compact=False):
         if not (1 <= b_r <= dh.n):
             raise ConfigError(f"tile size b_r={b_r} out of range for n={dh.n}")
         if b_r > MAX_TILE:
@@ -104,9 +159,14 @@ class GroupSolver:
         dev = dh.device
         f64 = dict(dtype=torch.float64, device=dev)
         self.X = torch.empty((self.ncol, self.n), **f64)
+        self.compact = bool(compact)
         self.c_re = torch.empty((self.ms, self.n), **f64)
-        self.c_im = torch.empty((self.ms, self.n), **f64)
-        self.s = torch.empty((self.ms, self.n), **f64)
+        if self.compact:  # Stewart codes: 1 real per real rotation, 2 per complex one
+            self.c_im = torch.empty((max(self.mc, 1), self.n), **f64)
+            self.s = None
+        else:
+            self.c_im = torch.empty((self.ms, self.n), **f64)
+            self.s = torch.empty((self.ms, self.n), **f64)
         self.seg_exp = torch.empty((self.N, self.ms), dtype=torch.int32, device=dev)
         self.alpha_exp = torch.empty(self.ms, dtype=torch.int32, device=dev)
         self.norms = torch.empty(self.ms, **f64)
@@ -126,7 +186,7 @@ class GroupSolver:
     def launch(self, B, broadcast, robust=True, mode="eigvec", stream=None, sync=True):
         """Enqueue the whole sweep.  B: device (n,) vector (broadcast) or (ncol, n)."""
         stream = stream or torch.cuda.current_stream(self.dh.device)
-        mode_i = {"solve": 0, "eigvec": 1}[mode]
+        mode_i = {"solve": 0, "eigvec": 1}[mode] | (MODE_COMPACT_ROTATIONS if self.compact else 0)
         args = (
             _ptr(self.dh.t), self.dh.ldh, self.n, self.b_r, _ptr(self.lam_re), _ptr(self.lam_im),
             self.mc, self.mr, _ptr(B), 0 if broadcast else self.n, 1 if broadcast else 0,
@@ -144,7 +204,7 @@ class GroupSolver:
     def output(self, nfail):
         return GroupOutput(self.X, self.c_re, self.c_im, self.s, self.seg_exp, self.alpha_exp,
                            self.norms, self.log2norm, self.fail, nfail, self.mc, self.mr,
-                           int(self.lib.hsrq_last_launch_count()))
+                           int(self.lib.hsrq_last_launch_count()), self.compact)
 
 
 @dataclass
@@ -288,7 +348,7 @@ def raise_first_failure(fail_codes, b_c, kinds):
 
 
 def solve_group(h, eigs_cplx, eigs_real, b, b_r, *, robust=True, mode="eigvec", b_c=32,
-                device=None, solver=None):
+                device=None, solver=None, compact=False):
     """Run one solve group; returns (GroupOutput, GroupSolver).
 
     ``b``: a real n-vector used for every column (the inverse-iteration
@@ -299,7 +359,7 @@ def solve_group(h, eigs_cplx, eigs_real, b, b_r, *, robust=True, mode="eigvec", 
     dh = DeviceHessenberg.of(hm, device)
     mc = len(np.atleast_1d(eigs_cplx)) if eigs_cplx is not None else 0
     mr = len(np.atleast_1d(eigs_real)) if eigs_real is not None else 0
-    gs = solver or GroupSolver(dh, b_r, mc, mr)
+    gs = solver or GroupSolver(dh, b_r, mc, mr, compact=compact)
     gs.set_shifts(eigs_cplx if mc else [], eigs_real if mr else [])
     bt = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64))
     broadcast = bt.dim() == 1

@@ -32,3 +32,10 @@ def same_blas(oracle):
     oracle.use_reference_blas(True)
     g = golden("solves")
     return str(g["corename"]) == oracle.blas_corename()
+
+
+def assert_bits(a, b, msg=""):
+    """Bitwise equality of float arrays (signed zeros and NaN payloads included)."""
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    assert a.shape == b.shape, (a.shape, b.shape, msg)
+    assert np.array_equal(a.view(np.int64), b.view(np.int64)), msg

@@ -114,3 +114,19 @@ def test_henry_bitwise(oracle):
         assert st == int(g[f"{t}_status"]), t
         if st == 0:
             np.testing.assert_array_equal(x, g[f"{t}_x"], err_msg=str(t))
+
+
+def test_compact_codes_bitwise(oracle):
+    """Stewart compact encode/decode (givens.py:90-198): oracle == reference."""
+    from conftest import assert_bits as eq
+
+    g = golden("compact")
+    eq(oracle.compact_encode(g["c"], g["s"]), g["t"])
+    dc, ds = oracle.compact_decode(g["t"])
+    eq(dc, g["dc"]), eq(ds, g["ds"])
+    t1, t2 = oracle.compact_encode(g["cre"], g["cs"], g["cim"])
+    eq(t1, g["packed"][0]), eq(t2, g["packed"][1])
+    dre, dim, dcs = oracle.compact_decode(g["packed"][0], g["packed"][1])
+    eq(dre, g["dre"]), eq(dim, g["dim"]), eq(dcs, g["dcs"])
+    kc, ks = oracle.compact_decode(g["codes"])
+    eq(kc, g["kc"]), eq(ks, g["ks"])

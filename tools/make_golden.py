@@ -411,6 +411,44 @@ def gen_henry():
     save("henry", tags=np.array(tags), **store)
 
 
+def gen_compact():
+    """Stewart compact rotation codes (givens.py:90-198) through the
+    reference's table functions (GivensTable.compact / from_compact,
+    core.py:193-209): rotations built by make_real / make_complex from random
+    and edge-case pairs, and raw codes across every window edge."""
+    from hessrq import givens
+
+    rng = np.random.default_rng(17)
+    a = rng.standard_normal(3000) * np.ldexp(1.0, rng.integers(-40, 40, 3000))
+    b = rng.standard_normal(3000) * np.ldexp(1.0, rng.integers(-40, 40, 3000))
+    a[:10] = [0.0, 1.0, -1.0, 0.0, 0.0, 2.0, -2.0, 3.0, 1e-300, 5.0]
+    b[:10] = [1.0, 0.0, 0.0, -1.0, 0.0, 2.0, 2.0, -3.0, 1.0, 1e-300]
+    rots = [givens.make_real(x, y) for x, y in zip(a, b)]
+    c = np.array([r.c for r in rots]).reshape(60, 50)
+    s_ = np.array([r.s for r in rots]).reshape(60, 50)
+    c[0, :6] = [-0.0, 0.0, -1.0, 1.0, 0.6, -0.6]
+    s_[0, :6] = [1.0, -1.0, -0.0, 0.0, 0.8, -0.8]
+    t = givens.compact_encode_table(c, s_)
+    dc, ds = givens.compact_decode_table(t)
+    v = (rng.standard_normal(3000) + 1j * rng.standard_normal(3000)) * np.ldexp(1.0, rng.integers(-30, 30, 3000))
+    v[:4] = [0.0, 1j, -1.0, 1e-300 + 0j]
+    a2 = a.copy()
+    a2[:4] = [1.0, 0.0, 0.5, 0.0]
+    crs = [givens.make_complex(x, y) for x, y in zip(a2, v)]
+    cre = np.array([r.c.real for r in crs]).reshape(60, 50)
+    cim = np.array([r.c.imag for r in crs]).reshape(60, 50)
+    cs = np.array([r.s for r in crs]).reshape(60, 50)
+    packed = givens.compact_encode_table_complex(cre, cim, cs)
+    dre, dim, dcs = givens.compact_decode_table_complex(packed)
+    codes = np.concatenate([rng.uniform(-7, 7, 2000),
+                            [0.0, -0.0, 1.0, -1.0, 2.0, -2.0, 3.0, -3.0, 4.0, -4.0, 5.0, -5.0,
+                             6.0, -6.0, 7.0, -7.0, np.nextafter(1.0, 2.0), np.nextafter(3.0, 4.0),
+                             np.nextafter(5.0, 6.0), 2.5, -6.25]])
+    kc, ks = givens.compact_decode_table(codes)
+    save("compact", c=c, s=s_, t=t, dc=dc, ds=ds, cre=cre, cim=cim, cs=cs, packed=packed,
+         dre=dre, dim=dim, dcs=dcs, codes=codes, kc=kc, ks=ks)
+
+
 def gen_runstats():
     """RunStats flops / formula per task type of reference solves (the bench
     CSV's flops_* and formula_* columns, cli.py:320-364)."""
@@ -451,6 +489,7 @@ if __name__ == "__main__":
         for name in sys.argv[1:]:
             globals()[f"gen_{name}"]()
         sys.exit(0)
+    gen_compact()
     gen_runstats()
     gen_henry()
     gen_backtransform()
