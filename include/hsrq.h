@@ -22,6 +22,9 @@
  *   hsrq_compact_encode / hsrq_compact_decode
  *                      GivensTable.compact / from_compact (core.py:193-209,
  *                      givens.py:90-198): Stewart's compact rotation codes
+ *   hsrq_hessenberg_reduce / hsrq_backmultiply
+ *                      householder_hessenberg (testprob.py:146-174) and
+ *                      z = Q0 x: the front end
  *   hsrq_protect_update_batch   protect_update, _kernels/numba_backend.py:47-67
  *   hsrq_hypot_batch            libm hypot as bound by numba (every rotation)
  *   hsrq_tile_diag              reduce_diag + solve_rsolve (numba_backend.py:
@@ -235,6 +238,26 @@ int64_t hsrq_compact_encode(int64_t count, int32_t cplx, const double* c_re, con
                             const double* s, double* t1, double* t2, void* stream);
 int64_t hsrq_compact_decode(int64_t count, int32_t cplx, const double* t1, const double* t2,
                             double* c_re, double* c_im, double* s, void* stream);
+
+/*
+ * Front end: H = Q^T A Q by Householder reflectors
+ * (householder_hessenberg, testprob.py:146-174: same reflectors, sign
+ * convention and skip rule -- columns already reduced are left untouched,
+ * so a Hessenberg input returns bit for bit with Q = I), blocked as in
+ * DGEHRD: panels of 64 reflectors, trailing updates as fp64 GEMMs.
+ *   A  in: n x n column-major (lda); out: H (zeros below the subdiagonal)
+ *   Q  out: n x n orthogonal (ldq), or NULL to skip accumulating it
+ *   ws >= hsrq_hessenberg_workspace_bytes(n) bytes of device memory
+ * Synchronises `stream`; returns 0 or a negative HSRQ_ERR_*.
+ * hsrq_backmultiply: Z = Q X (eigenvectors of H -> eigenvectors of A,
+ * PAPER.md:33-35); ncol real columns (a complex vector is two columns).
+ */
+size_t hsrq_hessenberg_workspace_bytes(int64_t n);
+int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, int64_t n,
+                               void* ws, size_t ws_bytes, void* stream);
+int64_t hsrq_backmultiply(const double* Q, int64_t ldq, int64_t n, const double* X, int64_t ldx,
+                          int64_t ncol, double* Z, int64_t ldz, void* stream);
+const char* hsrq_hessenberg_last_error(void);
 
 /* Elementwise device evaluations for bit-level parity of the scalar helpers. */
 int64_t hsrq_protect_update_batch(const double* bnorm, const double* hnorm, const double* xnorm,

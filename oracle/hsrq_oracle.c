@@ -1450,3 +1450,60 @@ void oracle_compact_decode(int64_t count, int cplx, const double* t1, const doub
         c_im[i] = ac * ds;
     }
 }
+
+/* ------------------------------------------------------------------ */
+/* Front end: householder_hessenberg, testprob.py:146-174 (unblocked)  */
+/* ------------------------------------------------------------------ */
+
+/* a: n x n column-major, overwritten by H; q: n x n column-major out (Q, with
+ * Q^T A Q = H).  Per column j: x = a[j+1:, j]; skipped when x[1:].x[1:] == 0;
+ * alpha = -sign(x0) hypot(x0, sqrt(tail)); v = (x - alpha e1)/||.||; the
+ * two-sided update with P = I - 2 v v^T and Q <- Q P. */
+void oracle_householder_hessenberg(int64_t n, double* a, double* q) {
+#define A_(i, j) a[(int64_t)(j) * n + (i)]
+#define Q_(i, j) q[(int64_t)(j) * n + (i)]
+    for (int64_t j = 0; j < n; j++)
+        for (int64_t i = 0; i < n; i++) Q_(i, j) = i == j ? 1.0 : 0.0;
+    double* v = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double* w = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    for (int64_t j = 0; j + 2 < n; j++) {
+        const int64_t m = n - j - 1;
+        double tail = 0.0;
+        for (int64_t r = 1; r < m; r++) tail += A_(j + 1 + r, j) * A_(j + 1 + r, j);
+        if (tail == 0.0) continue;
+        const double x0 = A_(j + 1, j);
+        const double nrm = hypot(x0, sqrt(tail));
+        const double alpha = x0 >= 0.0 ? -nrm : nrm;
+        double mx = 0.0, ss = 0.0;
+        for (int64_t r = 0; r < m; r++) {
+            v[r] = r == 0 ? x0 - alpha : A_(j + 1 + r, j);
+            if (fabs(v[r]) > mx) mx = fabs(v[r]);
+        }
+        for (int64_t r = 0; r < m; r++) ss += (v[r] / mx) * (v[r] / mx);
+        const double vn = mx * sqrt(ss);
+        for (int64_t r = 0; r < m; r++) v[r] /= vn;
+        /* left: a[j+1:, j:] -= 2 v (v^T a[j+1:, j:]) */
+        for (int64_t c = j; c < n; c++) {
+            double d = 0.0;
+            for (int64_t r = 0; r < m; r++) d += v[r] * A_(j + 1 + r, c);
+            for (int64_t r = 0; r < m; r++) A_(j + 1 + r, c) -= 2.0 * v[r] * d;
+        }
+        /* right: a[:, j+1:] -= 2 (a[:, j+1:] v) v^T ; q likewise */
+        for (int pass = 0; pass < 2; pass++) {
+            double* M = pass ? q : a;
+            for (int64_t i = 0; i < n; i++) {
+                double d = 0.0;
+                for (int64_t r = 0; r < m; r++) d += M[(j + 1 + r) * n + i] * v[r];
+                w[i] = d;
+            }
+            for (int64_t r = 0; r < m; r++)
+                for (int64_t i = 0; i < n; i++) M[(j + 1 + r) * n + i] -= 2.0 * w[i] * v[r];
+        }
+        A_(j + 1, j) = alpha;
+        for (int64_t r = j + 2; r < n; r++) A_(r, j) = 0.0;
+    }
+    free(v);
+    free(w);
+#undef A_
+#undef Q_
+}

@@ -303,3 +303,14 @@ def compact_decode(t1, t2=None):
     ci = np.empty_like(t1)
     L.oracle_compact_decode(ctypes.c_int64(t1.size), 1, _p(t1), _p(t2), _p(c), _p(ci), _p(s))
     return c, ci, s
+
+
+def householder_hessenberg(a):
+    """testprob.householder_hessenberg restated (unblocked, C): returns (H, Q)."""
+    L = lib()
+    h = np.array(a, dtype=np.float64, order="F")
+    n = h.shape[0]
+    q = np.empty((n, n), order="F")
+    L.oracle_householder_hessenberg.restype = None
+    L.oracle_householder_hessenberg(ctypes.c_int64(n), _p(h), _p(q))
+    return h, q

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhsrq_b200.so")
-SOURCES = [os.path.join(CSRC, "hsrq_kernels.cu")]
+SOURCES = [os.path.join(CSRC, "hsrq_kernels.cu"), os.path.join(CSRC, "hsrq_hessenberg.cu")]
 DEPS = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh")))
 DEPS.append(os.path.join(ROOT, "include", "hsrq.h"))
 
@@ -52,7 +52,7 @@ def build(force=False, verbose=False, variant=None, defines=()):
         return LIB
     extra = [f"-D{d}" for d in defines]
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp",
-           *SOURCES]
+           *SOURCES, "-lcublas"]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

@@ -54,6 +54,10 @@ SIGNATURES = {
     "hsrq_debug_counters": (_i64, [_p, _i32]),
     "hsrq_compact_encode": (_i64, [_i64, _i32, _p, _p, _p, _p, _p, _p]),
     "hsrq_compact_decode": (_i64, [_i64, _i32, _p, _p, _p, _p, _p, _p]),
+    "hsrq_hessenberg_workspace_bytes": (_sz, [_i64]),
+    "hsrq_hessenberg_reduce": (_i64, [_p, _i64, _p, _i64, _i64, _p, _sz, _p]),
+    "hsrq_backmultiply": (_i64, [_p, _i64, _i64, _p, _i64, _i64, _p, _i64, _p]),
+    "hsrq_hessenberg_last_error": (ctypes.c_char_p, []),
     "hsrq_henry_workspace_bytes": (_sz, [_i64, _i64, _i32]),
     "hsrq_henry_solve": (_i64, [_p, _i64, _i64, _p, _i64, _i32, _p, _i64, _p, _p, _sz, _p]),
 }

@@ -1,0 +1,285 @@
+// hsrq_hessenberg.cu -- the front end either side of the path (SURVEY §8(f)
+// row 2): orthogonal reduction of a dense matrix to upper Hessenberg form,
+// H = Q^T A Q (householder_hessenberg, testprob.py:146-174, DGEHRD-
+// equivalent), and the back-multiplication of eigenvectors of H into
+// eigenvectors of A, z = Q x.
+//
+// Same reflectors as the reference: for column j, x = A[j+1:, j], tail =
+// x[1:].x[1:], skipped when tail == 0 (so a Hessenberg input returns
+// unchanged with Q = I, bit for bit), alpha = -sign(x0) * hypot(x0,
+// sqrt(tail)), v = (x - alpha e1) / ||x - alpha e1||, P = I - 2 v v^T.
+// Applied blocked (the DGEHRD / DLAHR2 scheme): a panel of nb reflectors is
+// accumulated as Q_p = I - V T V^T with Y = A V T, so only the panel needs
+// the level-2 product A[:, j+1:] v per column (HBM-bound GEMV, the inherent
+// cost of the reduction); the trailing two-sided update and the Q update are
+// fp64 GEMMs (cuBLAS DGEMM, DMMA on sm_100a: plain library GEMMs).  The
+// per-column vector work -- the reflector with the reference's skip rule and
+// sign convention, the T column -- runs in one small kernel per column.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+
+#include "../../include/hsrq.h"
+#include "hsrq_device.cuh"
+
+namespace {
+
+constexpr int HB_THREADS = 1024;
+constexpr int HB_NB = 64;  // panel width
+
+thread_local char g_herr[256] = "";
+
+__device__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+  if (w == 0)
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (threadIdx.x == 0) red[32] = v;
+  __syncthreads();
+  return red[32];
+}
+
+__device__ double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+  if (w == 0)
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (threadIdx.x == 0) red[32] = v;
+  __syncthreads();
+  return red[32];
+}
+
+// Reflector of column j (testprob.py:160-172), one CTA.  a = column j of A
+// (length n, updated in place: a[j+1] = alpha, a[j+2:] = 0 unless skipped);
+// vcol = column i of V (length n: zero above row j+1); tau[i] / ntau[i] =
+// 2 / -2 (0 when skipped); T[i, i] = tau.
+__global__ void __launch_bounds__(HB_THREADS) k_reflector(double* a, int64_t n, int64_t j,
+                                                          double* vcol, double* tau, double* ntau,
+                                                          double* Tii) {
+  __shared__ double red[33];
+  const int64_t m = n - j - 1;  // x = a[j+1 : n]
+  const double* x = a + j + 1;
+  double t = 0.0;
+  for (int64_t r = 1 + threadIdx.x; r < m; r += blockDim.x) t += x[r] * x[r];
+  const double tail = block_sum(t, red);
+  const double x0 = x[0];
+  if (tail == 0.0) {  // column already reduced: identity reflector, nothing written
+    for (int64_t r = threadIdx.x; r < n; r += blockDim.x) vcol[r] = 0.0;
+    if (threadIdx.x == 0) {
+      *tau = 0.0;
+      *ntau = -0.0;
+      *Tii = 0.0;
+    }
+    return;
+  }
+  const double nrm = hsrq::ghypot(x0, sqrt(tail));
+  const double alpha = x0 >= 0.0 ? -nrm : nrm;
+  const double v0 = x0 - alpha;
+  // ||v|| scaled (v /= np.linalg.norm(v))
+  double mx = fabs(v0);
+  for (int64_t r = 1 + threadIdx.x; r < m; r += blockDim.x) mx = fmax(mx, fabs(x[r]));
+  mx = block_max(mx, red);
+  double ss = 0.0;
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) {
+    const double q = (r == 0 ? v0 : x[r]) / mx;
+    ss += q * q;
+  }
+  const double vn = mx * sqrt(block_sum(ss, red));
+  for (int64_t r = threadIdx.x; r < n; r += blockDim.x) {
+    double v = 0.0;
+    if (r > j) v = (r == j + 1 ? v0 : a[r]) / vn;
+    vcol[r] = v;
+  }
+  __syncthreads();  // every read of a[j+1:] precedes the writes below
+  for (int64_t r = j + 1 + threadIdx.x; r < n; r += blockDim.x) a[r] = r == j + 1 ? alpha : 0.0;
+  if (threadIdx.x == 0) {
+    *tau = 2.0;
+    *ntau = -2.0;
+    *Tii = 2.0;
+  }
+}
+
+__global__ void k_set_identity(double* Q, int64_t n, int64_t ldq) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n * n) return;
+  const int64_t c = t / n, r = t - c * n;
+  Q[c * ldq + r] = r == c ? 1.0 : 0.0;
+}
+
+struct Blas {
+  cublasHandle_t h = nullptr;
+  int dev = -1;
+};
+thread_local Blas g_blas;
+
+bool blas_ok(cublasStatus_t s, const char* what) {
+  if (s != CUBLAS_STATUS_SUCCESS) {
+    snprintf(g_herr, sizeof(g_herr), "%s: cublas status %d", what, (int)s);
+    return false;
+  }
+  return true;
+}
+bool cu_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    snprintf(g_herr, sizeof(g_herr), "%s: %s", what, cudaGetErrorString(e));
+    return false;
+  }
+  return true;
+}
+
+cublasHandle_t handle(cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (g_blas.h == nullptr || g_blas.dev != dev) {
+    if (cublasCreate(&g_blas.h) != CUBLAS_STATUS_SUCCESS) return nullptr;
+    g_blas.dev = dev;
+  }
+  cublasSetStream(g_blas.h, s);
+  cublasSetPointerMode(g_blas.h, CUBLAS_POINTER_MODE_HOST);
+  return g_blas.h;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hsrq_hessenberg_last_error(void) { return g_herr; }
+
+size_t hsrq_hessenberg_workspace_bytes(int64_t n) {
+  const size_t nb = HB_NB;
+  return sizeof(double) * ((size_t)n * nb * 2 + nb * nb + 4 * nb + nb * (size_t)n + 256);
+}
+
+int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, int64_t n,
+                               void* ws, size_t ws_bytes, void* stream_) {
+  if (n < 1 || lda < n || (Q && ldq < n)) return HSRQ_ERR_CONFIG;
+  if (ws_bytes < hsrq_hessenberg_workspace_bytes(n)) return HSRQ_ERR_WORKSPACE;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  cublasHandle_t h = handle(stream);
+  if (!h) {
+    snprintf(g_herr, sizeof(g_herr), "cublasCreate failed");
+    return HSRQ_ERR_CUDA;
+  }
+  const int nb = HB_NB;
+  double* V = (double*)ws;              // n x nb
+  double* Y = V + (size_t)n * nb;       // n x nb
+  double* T = Y + (size_t)n * nb;       // nb x nb (upper)
+  double* tau = T + (size_t)nb * nb;    // nb
+  double* ntau = tau + nb;              // nb
+  double* u = ntau + nb;                // nb
+  double* W = u + nb;                   // nb x n (also n x nb for the Q update)
+  const double one = 1.0, mone = -1.0, zero = 0.0;
+  if (Q) {
+    k_set_identity<<<(unsigned)((n * n + 255) / 256), 256, 0, stream>>>(Q, n, ldq);
+    if (!cu_ok(cudaGetLastError(), "identity")) return HSRQ_ERR_CUDA;
+  }
+  for (int64_t j0 = 0; j0 < n - 2; j0 += nb) {
+    const int pb = (int)std::min<int64_t>(nb, n - 2 - j0);
+    const int64_t L = n - j0 - 1;  // rows j0+1 .. n-1 (support of the panel's V)
+    if (!cu_ok(cudaMemsetAsync(T, 0, sizeof(double) * nb * nb, stream), "T"))
+      return HSRQ_ERR_CUDA;
+    for (int i = 0; i < pb; ++i) {
+      const int64_t j = j0 + i;
+      double* aj = A + j * lda;
+      if (i > 0) {
+        // right update of column j: a_j -= Y[:, :i] V[j, :i]^T
+        if (!blas_ok(cublasDgemv(h, CUBLAS_OP_N, (int)n, i, &mone, Y, (int)n, V + j, (int)n, &one,
+                                 aj, 1), "gemv right"))
+          return HSRQ_ERR_CUDA;
+        // left update of rows j0+1.. : a -= V T^T V^T a
+        if (!blas_ok(cublasDgemv(h, CUBLAS_OP_T, (int)L, i, &one, V + j0 + 1, (int)n, aj + j0 + 1,
+                                 1, &zero, u, 1), "gemv vta") ||
+            !blas_ok(cublasDtrmv(h, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, i,
+                                 T, nb, u, 1), "trmv") ||
+            !blas_ok(cublasDgemv(h, CUBLAS_OP_N, (int)L, i, &mone, V + j0 + 1, (int)n, u, 1, &one,
+                                 aj + j0 + 1, 1), "gemv left"))
+          return HSRQ_ERR_CUDA;
+      }
+      double* vi = V + (size_t)i * n;
+      k_reflector<<<1, HB_THREADS, 0, stream>>>(aj, n, j, vi, tau + i, ntau + i,
+                                                 T + (size_t)i * nb + i);
+      if (!cu_ok(cudaGetLastError(), "reflector")) return HSRQ_ERR_CUDA;
+      // Y[:, i] = tau (A[:, j+1:] v - Y[:, :i] (V^T v)); T[:i, i] = -tau T[:i, :i] (V^T v)
+      double* yi = Y + (size_t)i * n;
+      if (!blas_ok(cublasDgemv(h, CUBLAS_OP_N, (int)n, (int)(n - j - 1), &one, A + (j + 1) * lda,
+                               (int)lda, vi + j + 1, 1, &zero, yi, 1), "gemv Av"))
+        return HSRQ_ERR_CUDA;
+      if (i > 0) {
+        double* ti = T + (size_t)i * nb;
+        if (!blas_ok(cublasDgemv(h, CUBLAS_OP_T, (int)L, i, &one, V + j0 + 1, (int)n, vi + j0 + 1,
+                                 1, &zero, ti, 1), "gemv vtv") ||
+            !blas_ok(cublasDgemv(h, CUBLAS_OP_N, (int)n, i, &mone, Y, (int)n, ti, 1, &one, yi, 1),
+                     "gemv y") ||
+            !blas_ok(cublasDtrmv(h, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, i,
+                                 T, nb, ti, 1), "trmv t"))
+          return HSRQ_ERR_CUDA;
+        cublasSetPointerMode(h, CUBLAS_POINTER_MODE_DEVICE);
+        const bool ok = blas_ok(cublasDscal(h, i, ntau + i, ti, 1), "scal t");
+        cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST);
+        if (!ok) return HSRQ_ERR_CUDA;
+      }
+      cublasSetPointerMode(h, CUBLAS_POINTER_MODE_DEVICE);
+      const bool ok = blas_ok(cublasDscal(h, (int)n, tau + i, yi, 1), "scal y");
+      cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST);
+      if (!ok) return HSRQ_ERR_CUDA;
+    }
+    const int64_t c0 = j0 + pb, nc = n - c0;  // trailing columns
+    if (nc > 0) {
+      // right: A[:, c0:] -= Y V[c0:, :]^T
+      if (!blas_ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)nc, pb, &mone, Y, (int)n,
+                               V + c0, (int)n, &one, A + c0 * lda, (int)lda), "gemm right"))
+        return HSRQ_ERR_CUDA;
+      // left: A[j0+1:, c0:] -= V T^T (V^T A[j0+1:, c0:])
+      if (!blas_ok(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, pb, (int)nc, (int)L, &one, V + j0 + 1,
+                               (int)n, A + c0 * lda + j0 + 1, (int)lda, &zero, W, pb), "gemm vta") ||
+          !blas_ok(cublasDtrmm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
+                               CUBLAS_DIAG_NON_UNIT, pb, (int)nc, &one, T, nb, W, pb, W, pb),
+                   "trmm") ||
+          !blas_ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)L, (int)nc, pb, &mone, V + j0 + 1,
+                               (int)n, W, pb, &one, A + c0 * lda + j0 + 1, (int)lda), "gemm left"))
+        return HSRQ_ERR_CUDA;
+    }
+    if (Q) {
+      // Q[:, j0+1:] -= (Q[:, j0+1:] V T) V^T
+      if (!blas_ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, pb, (int)L, &one,
+                               Q + (j0 + 1) * ldq, (int)ldq, V + j0 + 1, (int)n, &zero, W, (int)n),
+                   "gemm qv") ||
+          !blas_ok(cublasDtrmm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                               CUBLAS_DIAG_NON_UNIT, (int)n, pb, &one, T, nb, W, (int)n, W, (int)n),
+                   "trmm q") ||
+          !blas_ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)L, pb, &mone, W, (int)n,
+                               V + j0 + 1, (int)n, &one, Q + (j0 + 1) * ldq, (int)ldq), "gemm q"))
+        return HSRQ_ERR_CUDA;
+    }
+  }
+  if (!cu_ok(cudaStreamSynchronize(stream), "sync")) return HSRQ_ERR_CUDA;
+  return 0;
+}
+
+int64_t hsrq_backmultiply(const double* Q, int64_t ldq, int64_t n, const double* X, int64_t ldx,
+                          int64_t ncol, double* Z, int64_t ldz, void* stream_) {
+  if (n < 1 || ncol < 0 || ldq < n || ldx < n || ldz < n) return HSRQ_ERR_CONFIG;
+  if (ncol == 0) return 0;
+  cublasHandle_t h = handle((cudaStream_t)stream_);
+  if (!h) return HSRQ_ERR_CUDA;
+  const double one = 1.0, zero = 0.0;
+  if (!blas_ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, (int)ncol, (int)n, &one, Q,
+                           (int)ldq, X, (int)ldx, &zero, Z, (int)ldz), "gemm qx"))
+    return HSRQ_ERR_CUDA;
+  return 0;
+}
+
+}  // extern "C"

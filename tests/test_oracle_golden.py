@@ -130,3 +130,36 @@ def test_compact_codes_bitwise(oracle):
     eq(dre, g["dre"]), eq(dim, g["dim"]), eq(dcs, g["dcs"])
     kc, ks = oracle.compact_decode(g["codes"])
     eq(kc, g["kc"]), eq(ks, g["ks"])
+
+
+def hessenberg_checks(a, h, q, ref_h=None, ref_q=None):
+    """SPEC bounds: ||Q^T Q - I|| <= 50 n eps, ||Q^T A Q - H|| <=
+    100 n eps ||A||, zeros below the subdiagonal; and, where the reduction is
+    forward-stable (no graded scaling), agreement with the reference's H, Q."""
+    n = a.shape[0]
+    eps = np.finfo(float).eps
+    na = max(np.linalg.norm(a), 1.0)
+    assert np.all(np.tril(h, -2) == 0.0)
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 50 * n * eps
+    assert np.linalg.norm(q.T @ a @ q - h) <= 100 * n * eps * na
+    if ref_h is not None:
+        assert np.linalg.norm(h - ref_h) <= 100 * n * eps * na
+        assert np.linalg.norm(q - ref_q) <= 100 * n * eps * np.sqrt(n)
+
+
+def test_householder_hessenberg_oracle(oracle):
+    """Front-end oracle vs the live reference: same reflectors (summation
+    order differs from numpy's BLAS, so agreement is to rounding); the skip
+    rule leaves an already-Hessenberg input bit-identical with Q = I.  The
+    graded case (last) is not forward-stable: backward-error bounds only."""
+    g = golden("hessenberg")
+    tags = list(g["tags"])
+    for t in tags:
+        a = g[f"{t}_a"]
+        h, q = oracle.householder_hessenberg(a)
+        fwd = t != tags[-1]
+        hessenberg_checks(a, h, q, g[f"{t}_h"] if fwd else None, g[f"{t}_q"] if fwd else None)
+        hessenberg_checks(a, g[f"{t}_h"], g[f"{t}_q"])  # the reference meets the same bounds
+    t = tags[9]  # random_unreduced: already Hessenberg
+    h, q = oracle.householder_hessenberg(g[f"{t}_a"])
+    assert np.array_equal(h, g[f"{t}_a"]) and np.array_equal(q, np.eye(h.shape[0]))

@@ -411,6 +411,37 @@ def gen_henry():
     save("henry", tags=np.array(tags), **store)
 
 
+def gen_hessenberg():
+    """householder_hessenberg (testprob.py:146-174) on dense inputs: random
+    matrices across the GPU panel width (64), an input that is already
+    Hessenberg (returned unchanged with Q = I), a column that is already
+    reduced mid-way (skip rule), graded rows, n = 1..3."""
+    from hessrq.testprob import householder_hessenberg
+
+    rng = np.random.default_rng(23)
+    store = {}
+    tags = []
+
+    def add(a):
+        hh, q = householder_hessenberg(a)
+        t = f"d{len(tags)}"
+        store[f"{t}_a"] = np.asfortranarray(a)
+        store[f"{t}_h"] = np.asfortranarray(hh)
+        store[f"{t}_q"] = np.asfortranarray(q)
+        tags.append(t)
+
+    for n in (1, 2, 3, 8, 50, 64, 65, 130, 200):
+        add(rng.standard_normal((n, n)))
+    add(np.array(random_unreduced(40, 2).data))
+    a = rng.standard_normal((90, 90))
+    a[12:, 10] = 0.0
+    a[71:, 69] = 0.0
+    add(a)
+    d = np.ldexp(1.0, np.arange(100) // 5)
+    add(rng.standard_normal((100, 100)) * d[:, None] / d[None, :])
+    save("hessenberg", tags=np.array(tags), **store)
+
+
 def gen_compact():
     """Stewart compact rotation codes (givens.py:90-198) through the
     reference's table functions (GivensTable.compact / from_compact,
@@ -489,6 +520,7 @@ if __name__ == "__main__":
         for name in sys.argv[1:]:
             globals()[f"gen_{name}"]()
         sys.exit(0)
+    gen_hessenberg()
     gen_compact()
     gen_runstats()
     gen_henry()
