@@ -8,6 +8,110 @@
 // broadcast lane by lane and every lane runs the same scalar recurrence, so
 // norms and vectors come out bit-identical to the oracle.
 
+// The ordered rotation sweep x[i-1] = c_i t1 - s_i t2, t1 = s_i t1 + c_i' t2
+// (rbacktransform :366-375 / crbacktransform :810-822).  Rows are loaded 32
+// at a time (lane = row), normalised / guarded, and their (x, c, s) are
+// broadcast lane by lane; the 32-step chunk is fully unrolled so the
+// shuffles issue ahead of the dependent t1 chain.  Lane t-1 keeps output row
+// base + t - 1; row base - 1 (the previous chunk's last) is written by lane 0.
+template <bool CP>
+__device__ __forceinline__ void bt_sweep(double* xr, double* xi, const double* cr,
+                                         const double* ci, const double* ss, int64_t n, int lane,
+                                         bool normalize, bool do_scale, double xmax, double rt,
+                                         double sc, int compact) {
+  double t1r = 0.0, t1i = 0.0;
+  // raw values of the next chunk, loaded one chunk ahead (latency hiding)
+  double ra = 0.0, rb = 0.0, rc = 1.0, rci = 0.0, rs = 0.0;
+  auto fetch = [&](int64_t i) {
+    if (i < n) {
+      ra = xr[i];
+      if (CP) rb = xi[i];
+      rc = cr[i];
+      if (CP) rci = ci[i];
+      if (!compact) rs = ss[i];
+    }
+  };
+  fetch(lane);
+  for (int64_t base = 0; base < n; base += 32) {
+    const int64_t i = base + lane;
+    double a = ra, b = rb, cc = 1.0, cim = 0.0, sv = 0.0;
+    const double c0 = rc, c1 = rci, c2 = rs;
+    fetch(base + 32 + lane);
+    if (i < n) {
+      if (normalize) {
+        a /= xmax;
+        a /= rt;
+        if (CP) {
+          b /= xmax;
+          b /= rt;
+        }
+      } else if (do_scale) {
+        a *= sc;
+        if (CP) b *= sc;
+      }
+      if (compact) {  // Stewart codes (givens.py:107-124, :144-149)
+        if (CP)
+          compact_decode_cplx(c0, c1, cc, cim, sv);
+        else
+          compact_decode(c0, cc, sv);
+      } else {
+        cc = c0;
+        sv = c2;
+        if (CP) cim = c1;
+      }
+    } else {
+      a = 0.0;
+      b = 0.0;
+    }
+    const int cnt = (int)(n - base < 32 ? n - base : 32);
+    if (base == 0) {  // t1 = x[0]
+      t1r = __shfl_sync(0xffffffffu, a, 0);
+      if (CP) t1i = __shfl_sync(0xffffffffu, b, 0);
+    }
+    double outr = 0.0, outi = 0.0;
+#pragma unroll
+    for (int t = 0; t < 32; t++) {
+      const double t2r = __shfl_sync(0xffffffffu, a, t);
+      const double t2i = CP ? __shfl_sync(0xffffffffu, b, t) : 0.0;
+      const double c_r = __shfl_sync(0xffffffffu, cc, t);
+      const double s_ = __shfl_sync(0xffffffffu, sv, t);
+      const double c_i = CP ? __shfl_sync(0xffffffffu, cim, t) : 0.0;
+      if (t < cnt && (t > 0 || base > 0)) {
+        double pr, pi = 0.0, nr, ni = 0.0;
+        if (CP) {
+          pr = (c_r * t1r - c_i * t1i) - s_ * t2r;
+          pi = (c_r * t1i + c_i * t1r) - s_ * t2i;
+          nr = s_ * t1r + (c_r * t2r + c_i * t2i);
+          ni = s_ * t1i + (c_r * t2i - c_i * t2r);
+        } else {
+          pr = c_r * t1r - s_ * t2r;
+          nr = c_r * t2r + s_ * t1r;
+        }
+        if (t == 0) {
+          if (lane == 0) {
+            xr[base - 1] = pr;
+            if (CP) xi[base - 1] = pi;
+          }
+        } else if (lane == t - 1) {
+          outr = pr;
+          outi = pi;
+        }
+        t1r = nr;
+        t1i = ni;
+      }
+    }
+    // lanes 0..cnt-2 hold final rows base..base+cnt-2
+    if (lane < cnt - 1) {
+      xr[base + lane] = outr;
+      if (CP) xi[base + lane] = outi;
+    }
+  }
+  if (lane == 0) {
+    xr[n - 1] = t1r;
+    if (CP) xi[n - 1] = t1i;
+  }
+}
+
 constexpr int BT_WARPS = 4;
 
 __global__ void __launch_bounds__(BT_WARPS * 32) k_backtransform(Ctx c, int32_t* alpha_exp,
@@ -80,20 +184,32 @@ __global__ void __launch_bounds__(BT_WARPS * 32) k_backtransform(Ctx c, int32_t*
     }
     // sum of squares in row order (:351-355)
     double tsum = 0.0;
+    double pa = 0.0, pb = 0.0;  // next chunk, loaded one chunk ahead
+    if (lane < n) {
+      pa = xr[lane];
+      if (cplx) pb = xi[lane];
+    }
     for (int64_t base = 0; base < n; base += 32) {
       const int64_t i = base + lane;
+      const double ca = pa, cb = pb;
+      if (i + 32 < n) {
+        pa = xr[i + 32];
+        if (cplx) pb = xi[i + 32];
+      }
       double sq = 0.0;
       if (i < n) {
         if (cplx) {
-          const double qr = xr[i] / xmax, qi = xi[i] / xmax;
+          const double qr = ca / xmax, qi = cb / xmax;
           sq = qr * qr + qi * qi;
         } else {
-          const double qv = xr[i] / xmax;
+          const double qv = ca / xmax;
           sq = qv * qv;
         }
       }
-      const int cnt = (int)(n - base < 32 ? n - base : 32);
-      for (int t = 0; t < cnt; t++) tsum += __shfl_sync(0xffffffffu, sq, t);
+      // rows >= n contribute +0.0: exact (tsum >= +0), so the chunk loop is
+      // fully unrolled and its shuffles issue ahead of the dependent adds
+#pragma unroll
+      for (int t = 0; t < 32; t++) tsum += __shfl_sync(0xffffffffu, sq, t);
     }
     rt = sqrt(tsum);
     int aout = amin;
@@ -115,82 +231,8 @@ __global__ void __launch_bounds__(BT_WARPS * 32) k_backtransform(Ctx c, int32_t*
     }
   }
   // normalise / guard and the rotation sweep, chunk by chunk (:358-375)
-  double t1r = 0.0, t1i = 0.0;
-  for (int64_t base = 0; base < n; base += 32) {
-    const int64_t i = base + lane;
-    double a = 0.0, b = 0.0, cc = 1.0, cim = 0.0, sv = 0.0;
-    if (i < n) {
-      a = xr[i];
-      if (cplx) b = xi[i];
-      if (normalize) {
-        a /= xmax;
-        a /= rt;
-        if (cplx) {
-          b /= xmax;
-          b /= rt;
-        }
-      } else if (do_scale) {
-        a *= sc;
-        if (cplx) b *= sc;
-      }
-      if (c.compact) {  // Stewart codes (givens.py:107-124, :144-149)
-        if (cplx)
-          compact_decode_cplx(cr[i], ci[i], cc, cim, sv);
-        else
-          compact_decode(cr[i], cc, sv);
-      } else {
-        cc = cr[i];
-        sv = ss[i];
-        if (cplx) cim = ci[i];
-      }
-    }
-    const int cnt = (int)(n - base < 32 ? n - base : 32);
-    double outr = 0.0, outi = 0.0;
-    for (int t = 0; t < cnt; t++) {
-      const double t2r = __shfl_sync(0xffffffffu, a, t);
-      const double t2i = cplx ? __shfl_sync(0xffffffffu, b, t) : 0.0;
-      if (base + t == 0) {  // t1 = x[0]
-        t1r = t2r;
-        t1i = t2i;
-        continue;
-      }
-      const double c_r = __shfl_sync(0xffffffffu, cc, t);
-      const double s_ = __shfl_sync(0xffffffffu, sv, t);
-      double nr, ni, pr, pi;
-      if (cplx) {
-        const double c_i = __shfl_sync(0xffffffffu, cim, t);
-        pr = (c_r * t1r - c_i * t1i) - s_ * t2r;
-        pi = (c_r * t1i + c_i * t1r) - s_ * t2i;
-        nr = s_ * t1r + (c_r * t2r + c_i * t2i);
-        ni = s_ * t1i + (c_r * t2i - c_i * t2r);
-      } else {
-        pr = c_r * t1r - s_ * t2r;
-        pi = 0.0;
-        nr = c_r * t2r + s_ * t1r;
-        ni = 0.0;
-      }
-      // x[i-1] = pr: row base+t-1 belongs to lane t-1 of this chunk, or to
-      // lane 31 of the previous chunk (written directly)
-      if (t == 0) {
-        if (lane == 0) {
-          xr[base - 1] = pr;
-          if (cplx) xi[base - 1] = pi;
-        }
-      } else if (lane == t - 1) {
-        outr = pr;
-        outi = pi;
-      }
-      t1r = nr;
-      t1i = ni;
-    }
-    // lanes 0..cnt-2 hold final rows base..base+cnt-2
-    if (lane < cnt - 1) {
-      xr[base + lane] = outr;
-      if (cplx) xi[base + lane] = outi;
-    }
-  }
-  if (lane == 0) {
-    xr[n - 1] = t1r;
-    if (cplx) xi[n - 1] = t1i;
-  }
+  if (cplx)
+    bt_sweep<true>(xr, xi, cr, ci, ss, n, lane, normalize, do_scale, xmax, rt, sc, c.compact);
+  else
+    bt_sweep<false>(xr, xi, cr, ci, ss, n, lane, normalize, do_scale, xmax, rt, sc, c.compact);
 }
