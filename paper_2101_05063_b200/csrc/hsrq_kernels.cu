@@ -305,20 +305,27 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 int g_panel_fast = 1;  // HSRQ_PANEL_FAST=0 forces the general epilogue (testing)
 
-// Diagonal-kernel variants: DP lanes per shift, DWR / DWC warps per CTA for
-// the real / complex kernel.  HSRQ_DIAG="DP,DWR,DWC" selects one of the
-// instantiated variants (tuning); the default is the measured best.
+// Diagonal-kernel variants: DP lanes per shift and DW warps per CTA, chosen
+// per kind (real / complex) from the number of shifts in the launch.  The
+// sweeps are latency-bound (a serial 128-step recurrence per shift), so the
+// best DP is the one that just fills the GPU: many shifts (one GPU, all of
+// config 5) -> few lanes per shift and more rows per lane; few shifts (a
+// rank's shard at 4 or 8 GPUs) -> more lanes per shift, shorter row loops.
+// Measured (tools/shard_time.py, config-5 shards): complex 6105 -> DP 4,
+// 3052 -> 8, 1526 and 763 -> 16/32.  HSRQ_DIAG="DP,DWR,DWC" forces one
+// (DP, real DW, complex DW) triple (tuning).
 struct DiagVariant {
-  int dp, dwr, dwc;
+  int dp, dw;
 };
-DiagVariant g_diag = {4, 4, 2};
+DiagVariant g_force_r = {0, 0}, g_force_c = {0, 0};
 
 template <int DP, int DW, bool CPLX>
 size_t diag_smem() {
   return sizeof(double) * (MAXK + DW * ((CPLX ? 4 : 2) * MAXK * (32 / DP) + 2 * MAXK));
 }
 
-#define HSRQ_DIAG_VARIANTS(X) X(4, 4, 2) X(8, 6, 4) X(16, 8, 8) X(2, 2, 1) X(4, 2, 1) X(4, 4, 4) X(4, 8, 4)
+#define HSRQ_DIAG_REAL(X) X(2, 2) X(4, 2) X(4, 4) X(4, 8) X(8, 6) X(16, 8) X(32, 8)
+#define HSRQ_DIAG_CPLX(X) X(2, 1) X(4, 1) X(4, 2) X(4, 4) X(8, 4) X(16, 8) X(32, 8)
 
 bool diag_attrs() {
   static bool done = false;
@@ -332,50 +339,77 @@ bool diag_attrs() {
   }
   const char* e = getenv("HSRQ_DIAG");
   if (e) {
-    DiagVariant v;
-    if (sscanf(e, "%d,%d,%d", &v.dp, &v.dwr, &v.dwc) == 3) g_diag = v;
+    int dp, dwr, dwc;
+    if (sscanf(e, "%d,%d,%d", &dp, &dwr, &dwc) == 3) {
+      g_force_r = DiagVariant{dp, dwr};
+      g_force_c = DiagVariant{dp, dwc};
+    }
   }
-  bool known = false;
-#define HSRQ_KNOWN(DP, DWR, DWC) known |= g_diag.dp == DP && g_diag.dwr == DWR && g_diag.dwc == DWC;
-  HSRQ_DIAG_VARIANTS(HSRQ_KNOWN)
-#undef HSRQ_KNOWN
-  if (!known) g_diag = DiagVariant{4, 4, 2};
   bool ok = true;
-#define HSRQ_ATTR(DP, DWR, DWC)                                                                  \
-  if (g_diag.dp == DP && g_diag.dwr == DWR && g_diag.dwc == DWC)                                 \
-    ok = ck(cudaFuncSetAttribute(k_diag_real<DP, DWR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                 (int)diag_smem<DP, DWR, false>()), "attr diag r") &&              \
-         ck(cudaFuncSetAttribute(k_diag_cplx<DP, DWC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                 (int)diag_smem<DP, DWC, true>()), "attr diag c");
-  HSRQ_DIAG_VARIANTS(HSRQ_ATTR)
-#undef HSRQ_ATTR
+#define HSRQ_ATTR_R(DP, DW)                                                                       ok = ok && ck(cudaFuncSetAttribute(k_diag_real<DP, DW>,                                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,                                                    (int)diag_smem<DP, DW, false>()), "attr diag r");
+#define HSRQ_ATTR_C(DP, DW)                                                                       ok = ok && ck(cudaFuncSetAttribute(k_diag_cplx<DP, DW>,                                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,                                                    (int)diag_smem<DP, DW, true>()), "attr diag c");
+  HSRQ_DIAG_REAL(HSRQ_ATTR_R)
+  HSRQ_DIAG_CPLX(HSRQ_ATTR_C)
+#undef HSRQ_ATTR_R
+#undef HSRQ_ATTR_C
   done = ok;
   return done;
 }
 
-template <int DP, int DWR_, int DWC_>
-void diag_launch_v(bool cplx, const Ctx& c, const DiagArgs& a, cudaStream_t s) {
-  const int64_t cnt = a.count;
-  if (cplx) {
-    const int per = DWC_ * (32 / DP);
-    k_diag_cplx<DP, DWC_><<<(unsigned)((cnt + per - 1) / per), DWC_ * 32,
-                            diag_smem<DP, DWC_, true>(), s>>>(c, a);
-  } else {
-    const int per = DWR_ * (32 / DP);
-    k_diag_real<DP, DWR_><<<(unsigned)((cnt + per - 1) / per), DWR_ * 32,
-                            diag_smem<DP, DWR_, false>(), s>>>(c, a);
+// Automatic choice: lanes per shift so that count * DP / 32 warps roughly
+// fill the machine (~6 warps per SM: the smem-limited residency of the
+// complex kernel at DP 4), rounded down to a power of two in [4, 32].
+DiagVariant diag_pick(bool cplx, int64_t count) {
+  const DiagVariant f = cplx ? g_force_c : g_force_r;
+  if (f.dp) return f;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const double want = 32.0 * 6.0 * sms / (double)(count > 0 ? count : 1);
+  int dp = 4;
+  while (dp < 32 && 2 * dp <= want) dp *= 2;
+  switch (dp) {
+    case 4: return cplx ? DiagVariant{4, 2} : DiagVariant{4, 4};
+    case 8: return cplx ? DiagVariant{8, 4} : DiagVariant{8, 6};
+    case 16: return DiagVariant{16, 8};
+    default: return DiagVariant{32, 8};
   }
 }
 
+template <int DP, int DW>
+void diag_launch_r(const Ctx& c, const DiagArgs& a, cudaStream_t s) {
+  const int per = DW * (32 / DP);
+  k_diag_real<DP, DW><<<(unsigned)((a.count + per - 1) / per), DW * 32,
+                        diag_smem<DP, DW, false>(), s>>>(c, a);
+}
+template <int DP, int DW>
+void diag_launch_c(const Ctx& c, const DiagArgs& a, cudaStream_t s) {
+  const int per = DW * (32 / DP);
+  k_diag_cplx<DP, DW><<<(unsigned)((a.count + per - 1) / per), DW * 32,
+                        diag_smem<DP, DW, true>(), s>>>(c, a);
+}
+
 void diag_launch(bool cplx, const Ctx& c, const DiagArgs& a, cudaStream_t s) {
-#define HSRQ_LAUNCH(DP, DWR, DWC)                                       \
-  if (g_diag.dp == DP && g_diag.dwr == DWR && g_diag.dwc == DWC) {      \
-    diag_launch_v<DP, DWR, DWC>(cplx, c, a, s);                         \
-    return;                                                             \
+  const DiagVariant v = diag_pick(cplx, a.count);
+#define HSRQ_LAUNCH_R(DP, DW)         \
+  if (v.dp == DP && v.dw == DW) {     \
+    diag_launch_r<DP, DW>(c, a, s);   \
+    return;                           \
   }
-  HSRQ_DIAG_VARIANTS(HSRQ_LAUNCH)
-#undef HSRQ_LAUNCH
-  diag_launch_v<4, 4, 2>(cplx, c, a, s);
+#define HSRQ_LAUNCH_C(DP, DW)         \
+  if (v.dp == DP && v.dw == DW) {     \
+    diag_launch_c<DP, DW>(c, a, s);   \
+    return;                           \
+  }
+  if (cplx) {
+    HSRQ_DIAG_CPLX(HSRQ_LAUNCH_C)
+    diag_launch_c<4, 2>(c, a, s);
+  } else {
+    HSRQ_DIAG_REAL(HSRQ_LAUNCH_R)
+    diag_launch_r<4, 4>(c, a, s);
+  }
+#undef HSRQ_LAUNCH_R
+#undef HSRQ_LAUNCH_C
 }
 
 struct WsLayout {
