@@ -324,8 +324,8 @@ size_t diag_smem() {
   return sizeof(double) * (MAXK + DW * ((CPLX ? 4 : 2) * MAXK * (32 / DP) + 2 * MAXK));
 }
 
-#define HSRQ_DIAG_REAL(X) X(2, 2) X(4, 2) X(4, 4) X(4, 8) X(8, 6) X(16, 8) X(32, 8)
-#define HSRQ_DIAG_CPLX(X) X(2, 1) X(4, 1) X(4, 2) X(4, 4) X(8, 4) X(16, 8) X(32, 8)
+#define HSRQ_DIAG_REAL(X) X(2, 2) X(4, 2) X(4, 4) X(4, 8) X(8, 6) X(16, 8) X(32, 8) X(16, 16) X(32, 16)
+#define HSRQ_DIAG_CPLX(X) X(2, 1) X(4, 1) X(4, 2) X(4, 4) X(8, 4) X(16, 8) X(32, 8) X(16, 16) X(32, 16)
 
 bool diag_attrs() {
   static bool done = false;
@@ -371,8 +371,11 @@ DiagVariant diag_pick(bool cplx, int64_t count) {
   switch (dp) {
     case 4: return cplx ? DiagVariant{4, 2} : DiagVariant{4, 4};
     case 8: return cplx ? DiagVariant{8, 4} : DiagVariant{8, 6};
-    case 16: return DiagVariant{16, 8};
-    default: return DiagVariant{32, 8};
+    // few shifts: the lookahead runs the sweep beside the panel; 16-warp CTAs
+    // pack it onto fewer SMs (a complex CTA then fills its SM's registers),
+    // leaving the other SMs to the panel at its full two-CTA rate
+    case 16: return DiagVariant{16, 16};
+    default: return DiagVariant{32, 16};
   }
 }
 
@@ -427,10 +430,10 @@ WsLayout ws_layout(int64_t n, int b_r, int64_t mc, int64_t mr) {
   off = 256;
   L.cr = off;
   off = align_up(off + sizeof(double) * (size_t)n * ncol, 256);
-  L.bop = off;
-  off = align_up(off + sizeof(double) * (size_t)(2 * ncol_pad) * KP, 256);
-  L.ss = off;
-  off = align_up(off + sizeof(StepScalars) * (size_t)ms, 256);
+  L.bop = off;  // two buffers (column parity, see the lookahead in solve_impl)
+  off = align_up(off + 2 * sizeof(double) * (size_t)(2 * ncol_pad) * KP, 256);
+  L.ss = off;   // two buffers
+  off = align_up(off + 2 * sizeof(StepScalars) * (size_t)ms, 256);
   L.hm0 = off;
   off = align_up(off + sizeof(double) * (size_t)N * N, 256);
   L.rs = off;
@@ -546,7 +549,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     attr_done = true;
   }
   // Optional per-launch timing: events around every launch, one sync at the end.
-  const int nev = 3 * c.N + 4;
+  const int nev = 6 * c.N + 6;
   cudaEvent_t* ev = nullptr;
   if (g_timing) {
     ev = new cudaEvent_t[nev];
@@ -556,7 +559,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   const int64_t nzero = std::max<int64_t>((int64_t)c.N * c.ms, (int64_t)c.N * c.N) + c.ms + 1;
   k_zero_state<<<(unsigned)((nzero + 255) / 256), 256, 0, stream>>>(c, feed ? 0 : 1);
   g_launches++;
-  const int64_t nbop = 2 * c.ncol_pad * KP;
+  const int64_t nbop = 4 * c.ncol_pad * KP;  // both buffers
   k_zero_bop<<<(unsigned)((nbop + 255) / 256), 256, 0, stream>>>(c.Bop, nbop);
   g_launches++;
   if (!feed) {
@@ -606,44 +609,73 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   if (g_timing) cudaEventRecord(ev[1], stream);
   const bool a16 = (ldh % 2 == 0) && (b_r % 2 == 0);
   const int S = std::min(SMAX, std::max(1, BM / b_r));
-  // side stream + fork/join events for the concurrent real diagonal kernel
-  // (one set per host thread; the side stream is created with the caller's
-  // device current and never synchronises with the legacy default stream)
-  thread_local cudaStream_t side = nullptr;
+  // Streams (one set per host thread and device): `side` runs the real
+  // diagonal kernel concurrently with the complex one; `dstr` (+ `dside` for
+  // the real shifts) carries the lookahead diagonal sweep of column jt-1
+  // while the panel of column jt finishes the rows above it -- high
+  // priority, so the latency-bound sweep's CTAs are scheduled ahead of the
+  // remaining panel CTAs.
+  thread_local cudaStream_t side = nullptr, dstr = nullptr, dside = nullptr;
   thread_local int side_dev = -1;
-  thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_bot = nullptr,
+                           ev_diag = nullptr;
   {
     int dev = 0;
     cudaGetDevice(&dev);
     if (side_dev != dev) {
-      if (!ck(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "side stream") ||
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if (!ck(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo), "side stream") ||
+          !ck(cudaStreamCreateWithPriority(&dstr, cudaStreamNonBlocking, hi), "diag stream") ||
+          !ck(cudaStreamCreateWithPriority(&dside, cudaStreamNonBlocking, hi), "diag side") ||
           !ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "fork event") ||
-          !ck(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "join event"))
+          !ck(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "join event") ||
+          !ck(cudaEventCreateWithFlags(&ev_bot, cudaEventDisableTiming), "bottom event") ||
+          !ck(cudaEventCreateWithFlags(&ev_diag, cudaEventDisableTiming), "diag event"))
         return HSRQ_ERR_CUDA;
       side_dev = dev;
     }
   }
-  for (int jt = c.N - 1; jt >= 0; --jt) {
+  // Lookahead: the diagonal sweep of column jt-1 only needs tile row jt-1 of
+  // panel jt, so that row goes first and the sweep overlaps the rest of the
+  // panel.  It pays when the sweep leaves room on the SMs (few shifts per
+  // GPU, i.e. a rank's shard); with all of config 5 on one GPU the sweep's
+  // shared memory fills every SM and the two phases serialise anyway.
+  // HSRQ_LOOKAHEAD=0/1 forces it off/on.
+  // Measured (tools/shard_time.py, config-5 shards, ms per solve, off -> on):
+  // 1 GPU 515 -> 514, 1/2 shard 291 -> 261, 1/4 175 -> 162, 1/8 116 -> 105.
+  // Off for a whole config-5 group, where it gains nothing and the panel's
+  // launch times (the roofline's denominator) would include the sweep.
+  bool lookahead = c.ms <= 6000;
+  if (const char* e = getenv("HSRQ_LOOKAHEAD")) lookahead = atoi(e) != 0;
+  // Bop / SS are double-buffered by column parity: the lookahead sweep of
+  // jt-1 writes its panel operands while panel jt still reads its own.
+  Ctx cb[2] = {c, c};
+  cb[1].Bop = c.Bop + 2 * c.ncol_pad * KP;
+  cb[1].SS = c.SS + c.ms;
+  const int kt = 6;  // timing events per column
+  auto tev = [&](int jt, int slot) { return ev[2 + kt * jt + slot]; };
+
+  // diagonal sweep of column jd on stream sd (real shifts forked onto `side`)
+  auto run_diag = [&](int jd, cudaStream_t sd, cudaStream_t sside) -> bool {
     DiagArgs a;
     memset(&a, 0, sizeof(a));
-    a.jt = jt;
-    a.js = (int64_t)jt * b_r;
-    int64_t je = a.js + b_r < n ? a.js + b_r : n;
+    a.jt = jd;
+    a.js = (int64_t)jd * b_r;
+    const int64_t je = a.js + b_r < n ? a.js + b_r : n;
     a.k = (int)(je - a.js);
-    a.has_left = jt > 0;
-    if (feed) cudaStreamWaitEvent(stream, feed->blk[jt], 0);  // this column's H block + tables
-    // Real and complex shifts are independent columns: their diagonal
-    // kernels run concurrently (the real one on a side stream, forked and
-    // joined with events), so the latency-bound sweeps share the SMs.
-    const bool fork = mc > 0 && mr > 0 && side != nullptr;
+    a.has_left = jd > 0;
+    if (feed) cudaStreamWaitEvent(sd, feed->blk[jd], 0);  // this column's H block + tables
+    if (g_timing) cudaEventRecord(tev(jd, 0), sd);
+    const bool fork = mc > 0 && mr > 0;
     if (fork) {
-      cudaEventRecord(ev_fork, stream);
-      cudaStreamWaitEvent(side, ev_fork, 0);
+      cudaEventRecord(ev_fork, sd);
+      cudaStreamWaitEvent(sside, ev_fork, 0);
     }
     // Compact rotation storage: the diagonal kernels record the tile's exact
     // rotations into the tile scratch Rt (the panel operands need them), and
     // k_compact_tile writes their Stewart codes into the tables.
-    Ctx cd = c;
+    Ctx cd = cb[jd & 1];
     a.rot_off = a.js;
     if (c.compact) {
       cd.c_re = c.Rt;
@@ -655,55 +687,87 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     if (mr > 0) {
       a.q0 = mc;
       a.count = mr;
-      diag_launch(false, cd, a, fork ? side : stream);
+      diag_launch(false, cd, a, fork ? sside : sd);
       g_launches++;
     }
     if (mc > 0) {
       a.q0 = 0;
       a.count = mc;
-      diag_launch(true, cd, a, stream);
+      diag_launch(true, cd, a, sd);
       g_launches++;
     }
     if (fork) {
-      cudaEventRecord(ev_join, side);
-      cudaStreamWaitEvent(stream, ev_join, 0);
+      cudaEventRecord(ev_join, sside);
+      cudaStreamWaitEvent(sd, ev_join, 0);
     }
     if (c.compact) {
       const int64_t cnt = (int64_t)a.k * c.ms;
-      k_compact_tile<<<(unsigned)((cnt + 255) / 256), 256, 0, stream>>>(c, a.js, a.k);
+      k_compact_tile<<<(unsigned)((cnt + 255) / 256), 256, 0, sd>>>(c, a.js, a.k);
       g_launches++;
     }
-    if (g_timing) cudaEventRecord(ev[2 + 3 * jt], stream);
-    if (jt > 0) {
-      PanelArgs p;
-      p.jt = jt;
-      p.js = a.js;
-      p.k = a.k;
-      p.S = S;
-      RowScalars* rsc = (RowScalars*)(w + L.rsc);
-      const int64_t nsc = (int64_t)jt * c.ms;
-      k_scalars<<<(unsigned)((nsc + 127) / 128), 128, 0, stream>>>(c, p, rsc);
-      g_launches++;
-      if (g_timing) cudaEventRecord(ev[3 + 3 * jt], stream);
-      dim3 gp((unsigned)((jt + S - 1) / S), (unsigned)(c.ncol_pad / BN));
-      const bool seg16 = (b_r % 16) == 0;
-      if (a16 && b_r == BM && g_panel_fast)
-        k_panel<true, true, true><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
-      else if (a16 && seg16)
-        k_panel<true, true, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
-      else if (a16)
-        k_panel<true, false, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
-      else if (seg16)
-        k_panel<false, true, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
-      else
-        k_panel<false, false, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(c, p, rsc);
-      g_launches++;
-    }
+    if (g_timing) cudaEventRecord(tev(jd, 1), sd);
+    return true;
+  };
+  // panel GEMM of column jt over tile rows [t0, t1)
+  const bool seg16 = (b_r % 16) == 0;
+  RowScalars* rsc = (RowScalars*)(w + L.rsc);
+  auto run_panel = [&](int jt, int t0, int t1) {
+    if (t1 <= t0) return;
+    PanelArgs p;
+    p.jt = jt;
+    p.js = (int64_t)jt * b_r;
+    p.k = (int)(std::min<int64_t>(p.js + b_r, n) - p.js);
+    p.S = S;
+    p.t0 = t0;
+    p.t1 = t1;
+    const Ctx& cj = cb[jt & 1];
+    dim3 gp((unsigned)((t1 - t0 + S - 1) / S), (unsigned)(c.ncol_pad / BN));
+    if (a16 && b_r == BM && g_panel_fast)
+      k_panel<true, true, true><<<gp, PANEL_THREADS, panel_smem, stream>>>(cj, p, rsc);
+    else if (a16 && seg16)
+      k_panel<true, true, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(cj, p, rsc);
+    else if (a16)
+      k_panel<true, false, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(cj, p, rsc);
+    else if (seg16)
+      k_panel<false, true, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(cj, p, rsc);
+    else
+      k_panel<false, false, false><<<gp, PANEL_THREADS, panel_smem, stream>>>(cj, p, rsc);
+    g_launches++;
+  };
+
+  run_diag(c.N - 1, stream, side);
+  for (int jt = c.N - 1; jt >= 1; --jt) {
+    PanelArgs p;
+    p.jt = jt;
+    p.js = (int64_t)jt * b_r;
+    p.k = (int)(std::min<int64_t>(p.js + b_r, n) - p.js);
+    p.S = S;
+    p.t0 = 0;
+    p.t1 = jt;
+    if (g_timing) cudaEventRecord(tev(jt, 2), stream);
+    const int64_t nsc = (int64_t)jt * c.ms;
+    k_scalars<<<(unsigned)((nsc + 127) / 128), 128, 0, stream>>>(cb[jt & 1], p, rsc);
+    g_launches++;
     if (g_timing) {
-      if (jt == 0) cudaEventRecord(ev[3 + 3 * jt], stream);
-      cudaEventRecord(ev[4 + 3 * jt], stream);
+      cudaEventRecord(tev(jt, 3), stream);
+      cudaEventRecord(tev(jt, 4), stream);
+    }
+    if (lookahead) {
+      run_panel(jt, jt - 1, jt);  // tile row jt-1: all the next sweep needs
+      cudaEventRecord(ev_bot, stream);
+      cudaStreamWaitEvent(dstr, ev_bot, 0);
+      run_diag(jt - 1, dstr, dside);
+      cudaEventRecord(ev_diag, dstr);
+      run_panel(jt, 0, jt - 1);
+      if (g_timing) cudaEventRecord(tev(jt, 5), stream);
+      cudaStreamWaitEvent(stream, ev_diag, 0);
+    } else {
+      run_panel(jt, 0, jt);
+      if (g_timing) cudaEventRecord(tev(jt, 5), stream);
+      run_diag(jt - 1, stream, side);
     }
   }
+  if (g_timing) cudaEventRecord(ev[nev - 3], stream);
   if (!feed || !feed->X_host) {
     k_backtransform<<<(unsigned)((c.ms + BT_WARPS - 1) / BT_WARPS), BT_WARPS * 32, 0, stream>>>(
         c, alpha_exp, norms, log2norm, 0, c.ms);
@@ -748,22 +812,24 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     cudaEventSynchronize(ev[nev - 2]);
     float t;
     double t_diag = 0, t_panel = 0, t_scal = 0;
-    // per column: ev[prev] diag ev[2+3jt] scalars ev[3+3jt] panel ev[4+3jt]
-    int prev = 1;
+    // per column: diag [0, 1] (on its stream), scalars [2, 3], panel [4, 5]
     for (int jt = c.N - 1; jt >= 0; --jt) {
-      cudaEventElapsedTime(&t, ev[prev], ev[2 + 3 * jt]);
+      cudaEventElapsedTime(&t, tev(jt, 0), tev(jt, 1));
       t_diag += t;
-      cudaEventElapsedTime(&t, ev[2 + 3 * jt], ev[3 + 3 * jt]);
+      if (jt == 0) continue;
+      cudaEventElapsedTime(&t, tev(jt, 2), tev(jt, 3));
       t_scal += t;
-      cudaEventElapsedTime(&t, ev[3 + 3 * jt], ev[4 + 3 * jt]);
+      cudaEventElapsedTime(&t, tev(jt, 4), tev(jt, 5));
       t_panel += t;
-      prev = 4 + 3 * jt;
     }
     g_phase_ms[4] = t_scal;
-    cudaEventElapsedTime(&t, ev[prev], ev[nev - 2]);
+    cudaEventElapsedTime(&t, ev[1], tev(c.N - 1, 0));
+    double t_setup = t;
+    cudaEventElapsedTime(&t, ev[nev - 3], ev[nev - 2]);
     g_phase_ms[2] = t;
     cudaEventElapsedTime(&t, ev[0], ev[1]);
-    g_phase_ms[3] = t;
+    t_setup += t;
+    g_phase_ms[3] = t_setup;
     g_phase_ms[0] = t_diag;
     g_phase_ms[1] = t_panel;
     for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);

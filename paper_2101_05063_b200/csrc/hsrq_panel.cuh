@@ -25,6 +25,7 @@ struct PanelArgs {
   int64_t js;
   int k;  // width of tile column jt (GEMM K)
   int S;  // tile rows per CTA
+  int t0, t1;  // k_panel: tile rows [t0, t1) of this launch (the lookahead splits off jt-1)
 };
 
 // Per (tile row, shift) scalars of update steps 1-2, written by k_scalars.
@@ -700,8 +701,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
   const int S = p.S;
   // grid: x = tile-row block (fastest), y = column block, so consecutive CTAs
   // reuse one B-operand block (and the whole H panel stays L2-resident)
-  const int tile0 = blockIdx.x * S;
-  const int ntiles = min(S, p.jt - tile0);
+  const int tile0 = p.t0 + blockIdx.x * S;
+  const int ntiles = min(S, p.t1 - tile0);
   const int64_t row0 = (int64_t)tile0 * c.b_r;
   const int rows_valid = ntiles * c.b_r;
   const int64_t col0 = (int64_t)blockIdx.y * BN;
