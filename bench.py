@@ -270,12 +270,10 @@ def run_gpu(args):
         for _ in range(args.steps):
             step(timing=True)
             launches += int(lib.hsrq_last_launch_count())
-            pt = np.zeros(5)
-            lib.hsrq_phase_times(ctypes.c_void_p(pt.ctypes.data))
-            phase += pt
             gather()
         e1.record(stream)
         torch.cuda.synchronize()
+    lib.hsrq_phase_times(ctypes.c_void_p(phase.ctypes.data))  # summed over the K timed steps
     ms = e0.elapsed_time(e1) / args.steps
     t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -416,6 +414,8 @@ def run_gpu(args):
     }
     if e2e:
         line["e2e"] = e2e
+    if world == 1 and not args.no_shards:
+        line["shard_projection"] = shard_projection(dh, b_r, er, ec, start, stream)
     if world == 1 and not args.no_cpu:
         cnt, dt, threads, sample = cpu_sample(h, er, ec, b_r, args.cpu_real, args.cpu_cplx)
         line["cpu_baseline"] = {"value": cnt / dt, "unit": "eigenvectors/s", "cores": threads,
@@ -426,6 +426,42 @@ def run_gpu(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def shard_projection(dh, b_r, er, ec, start, stream, worlds=(1, 2, 4, 8), reps=3):
+    """Strong-scaling evidence on one GPU: the per-rank time of rank 0's shard
+    (parallel.shard_bounds: an equal share of each kind) for a W-way
+    partition, run alone.  Ranks never wait on one another inside the sweep
+    (H replicated, no collective until the final gather of X), so this is
+    the rank's compute time; the NCCL gather (~2 GB of X into rank 0 over
+    NVLink, a few ms) is not included."""
+    import torch
+
+    from paper_2101_05063_b200.solver import GroupSolver
+
+    out = {}
+    for W in worlds:
+        my_r, my_c = partition(er, ec, 0, W)
+        gs = GroupSolver(dh, b_r, my_c.size, my_r.size)
+        gs.set_shifts(my_c, my_r)
+        gs.launch(start, True, stream=stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            gs.launch(start, True, stream=stream, sync=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / reps
+        if W == 1:
+            ms1 = t
+        out[str(W)] = {"shard": f"{my_r.size} real + {my_c.size} complex shifts",
+                       "ms_per_step": t, "projected_efficiency": ms1 / (W * t)}
+        del gs
+        torch.cuda.empty_cache()
+    out["note"] = ("per-rank time of rank 0's W-way shard measured alone on this GPU, launches "
+                   "pipelined without per-phase events (W=1 is the base); no collective "
+                   "inside the sweep; excludes the final NCCL gather of X")
+    return out
 
 
 def _offdiag_update(n, b_r, cplx):
@@ -452,6 +488,7 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override n (debug; eigvals computed live)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-shards", action="store_true", help="skip the 2/4/8-way shard projection")
     ap.add_argument("--cpu-real", type=int, default=16)
     ap.add_argument("--cpu-cplx", type=int, default=16)
     args = ap.parse_args()

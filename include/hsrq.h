@@ -164,9 +164,13 @@ int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset);
 /* Kernel launches issued by the last solve on this thread (for accounting). */
 int64_t hsrq_last_launch_count(void);
 
-/* Per-phase device times (ms) of the last solve run with timing enabled:
+/* Per-phase device times (ms), summed over the solves run with timing
+ * enabled since the previous call (which this call waits for):
  * out_host[0] = diagonal kernels, [1] = panel GEMM kernels (k_panel), [2] =
- * backtransform, [3] = setup, [4] = guard-scalar kernels (k_scalars).  Enable with hsrq_set_timing(1) (adds events, serialises). */
+ * backtransform, [3] = setup, [4] = guard-scalar kernels (k_scalars).
+ * Enable with hsrq_set_timing(1): events around every phase, read back
+ * here, so a timed solve is not synchronised by the timing itself.  With
+ * the lookahead schedule the diagonal and panel intervals overlap. */
 void hsrq_set_timing(int32_t enable);
 void hsrq_phase_times(double* out_host);
 

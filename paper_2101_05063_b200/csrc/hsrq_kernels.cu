@@ -292,6 +292,43 @@ thread_local int64_t g_launches = 0;
 int g_timing = 0;
 unsigned long long* g_tl = nullptr;
 double g_phase_ms[5] = {0, 0, 0, 0, 0};
+// Timed solves whose events have not been read yet (hsrq_phase_times).
+// Per solve: ev[0] start, ev[1] after setup, per column jt the six events
+// 2 + 6 jt + {diag start, diag end, scalars start/end, panel start/end},
+// ev[nev - 3] / ev[nev - 2] around the backtransform.
+struct PendingTiming {
+  cudaEvent_t* ev;
+  int nev, N;
+};
+std::vector<PendingTiming> g_pending;
+
+void drain_timing(double* acc) {
+  for (PendingTiming& pt : g_pending) {
+    cudaEvent_t* ev = pt.ev;
+    const int nev = pt.nev;
+    auto tev = [&](int jt, int slot) { return ev[2 + 6 * jt + slot]; };
+    cudaEventSynchronize(ev[nev - 2]);
+    float t;
+    for (int jt = pt.N - 1; jt >= 0; --jt) {
+      cudaEventElapsedTime(&t, tev(jt, 0), tev(jt, 1));
+      acc[0] += t;
+      if (jt == 0) continue;
+      cudaEventElapsedTime(&t, tev(jt, 2), tev(jt, 3));
+      acc[4] += t;
+      cudaEventElapsedTime(&t, tev(jt, 4), tev(jt, 5));
+      acc[1] += t;
+    }
+    cudaEventElapsedTime(&t, ev[nev - 3], ev[nev - 2]);
+    acc[2] += t;
+    cudaEventElapsedTime(&t, ev[0], ev[1]);
+    acc[3] += t;
+    cudaEventElapsedTime(&t, ev[1], tev(pt.N - 1, 0));
+    acc[3] += t;
+    for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
+    delete[] ev;
+  }
+  g_pending.clear();
+}
 
 bool ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
@@ -808,32 +845,9 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     cudaStreamWaitEvent(stream, feed->blk[c.N + 1], 0);  // X is on the host
   }
   if (g_timing) {
+    // read back lazily (hsrq_phase_times): no host sync inside a timed solve
     cudaEventRecord(ev[nev - 2], stream);
-    cudaEventSynchronize(ev[nev - 2]);
-    float t;
-    double t_diag = 0, t_panel = 0, t_scal = 0;
-    // per column: diag [0, 1] (on its stream), scalars [2, 3], panel [4, 5]
-    for (int jt = c.N - 1; jt >= 0; --jt) {
-      cudaEventElapsedTime(&t, tev(jt, 0), tev(jt, 1));
-      t_diag += t;
-      if (jt == 0) continue;
-      cudaEventElapsedTime(&t, tev(jt, 2), tev(jt, 3));
-      t_scal += t;
-      cudaEventElapsedTime(&t, tev(jt, 4), tev(jt, 5));
-      t_panel += t;
-    }
-    g_phase_ms[4] = t_scal;
-    cudaEventElapsedTime(&t, ev[1], tev(c.N - 1, 0));
-    double t_setup = t;
-    cudaEventElapsedTime(&t, ev[nev - 3], ev[nev - 2]);
-    g_phase_ms[2] = t;
-    cudaEventElapsedTime(&t, ev[0], ev[1]);
-    t_setup += t;
-    g_phase_ms[3] = t_setup;
-    g_phase_ms[0] = t_diag;
-    g_phase_ms[1] = t_panel;
-    for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
-    delete[] ev;
+    g_pending.push_back(PendingTiming{ev, nev, c.N});
   }
   if (!ck(cudaGetLastError(), "launch")) return HSRQ_ERR_CUDA;
   return 0;
@@ -1076,6 +1090,8 @@ int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset) {
 }
 void hsrq_set_timing(int32_t enable) { g_timing = enable; }
 void hsrq_phase_times(double* out_host) {
+  for (int i = 0; i < 5; i++) g_phase_ms[i] = 0.0;
+  drain_timing(g_phase_ms);
   for (int i = 0; i < 5; i++) out_host[i] = g_phase_ms[i];
 }
 

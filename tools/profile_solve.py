@@ -48,6 +48,7 @@ for _ in range(a.reps):
 torch.cuda.synchronize()
 pt = np.zeros(5)
 L.hsrq_phase_times(ctypes.c_void_p(pt.ctypes.data))
+pt /= max(1, a.reps)
 L.hsrq_set_timing(0)
 print("failed", nf, "phase ms (diag, panel, backtransform, setup, scalars):", np.round(pt, 2).tolist())
 cnt = np.zeros(16, dtype=np.int64)
