@@ -113,3 +113,17 @@ def test_bench_csv_inputs_and_header(tmp_path):
     pt = tmp_path / "m.txt"
     pt.write_text(f"{a.shape[0]}\n" + "\n".join(" ".join(repr(float(v)) for v in row) for row in a))
     assert np.array_equal(benchcsv.read_matrix(str(pt)).data, a)
+
+
+def test_verify_suite_matrices_match_reference_fixtures():
+    """verify.paper_h restates the paper's H2 / H3 (§5.2) exactly: the golden
+    solves' gen_h2(60) / gen_h3(60) matrices."""
+    from conftest import golden
+    from paper_2101_05063_b200.verify import paper_h
+
+    g = golden("solves")
+    hs = {tuple(np.asarray(g[f"{t}_h"]).ravel()[:3]): np.asarray(g[f"{t}_h"]) for t in g["tags"]
+          if np.asarray(g[f"{t}_h"]).shape == (60, 60)}
+    h2, h3 = paper_h(60, -60).data, paper_h(60, 0.5).data
+    assert any(np.array_equal(h, h2) for h in hs.values())
+    assert any(np.array_equal(h, h3) for h in hs.values())
