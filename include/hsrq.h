@@ -158,6 +158,28 @@ int64_t hsrq_solve_group_host(const double* H, int64_t ldh, int64_t n, int32_t b
                               double* norms, double* log2norm, int64_t* fail, int32_t robust,
                               int32_t mode, void* dev_ws, size_t dev_ws_bytes, void* stream);
 
+/*
+ * Asynchronous host-buffer solve: the same arguments and results as
+ * hsrq_solve_group_host, but the call returns a ticket (>= 0) as soon as
+ * everything is enqueued; hsrq_host_wait(ticket) waits for that solve's
+ * outputs to be on the host and returns its number of failed shifts.  X and
+ * the small outputs travel on their own D2H stream, so a caller that keeps
+ * two solves in flight (two device workspaces, two sets of host outputs)
+ * downloads solve i while solve i+1 sweeps -- how hsrq3in's w_max groups or
+ * a stream of solve groups hide the transfers.  The upload of H starts at
+ * once (it does not wait for earlier work on `stream`), so a device
+ * workspace may only be passed again after the ticket of its previous solve
+ * has been waited.  At most 16 tickets are outstanding per host thread.
+ */
+int64_t hsrq_solve_group_host_async(const double* H, int64_t ldh, int64_t n, int32_t b_r,
+                                    const double* lam_re, const double* lam_im, int64_t m_cplx,
+                                    int64_t m_real, const double* B, int64_t ldb,
+                                    int32_t b_broadcast, double* X, int64_t ldx, int32_t* seg_exp,
+                                    int32_t* alpha_exp, double* norms, double* log2norm,
+                                    int64_t* fail, int32_t robust, int32_t mode, void* dev_ws,
+                                    size_t dev_ws_bytes, void* stream);
+int64_t hsrq_host_wait(int64_t ticket);
+
 /* Guard-path event counters (diagnostics): out_host[16]; reset != 0 zeroes them. */
 int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset);
 

@@ -40,6 +40,12 @@ SIGNATURES = {
         [_p, _i64, _i64, _i32, _p, _p, _i64, _i64, _p, _i64, _i32, _p, _i64, _p, _p, _p, _p, _p,
          _i32, _i32, _p, _sz, _p],
     ),
+    "hsrq_solve_group_host_async": (
+        _i64,
+        [_p, _i64, _i64, _i32, _p, _p, _i64, _i64, _p, _i64, _i32, _p, _i64, _p, _p, _p, _p, _p,
+         _i32, _i32, _p, _sz, _p],
+    ),
+    "hsrq_host_wait": (_i64, [_i64]),
     "hsrq_last_launch_count": (_i64, []),
     "hsrq_set_timing": (None, [_i32]),
     "hsrq_phase_times": (None, [_p]),

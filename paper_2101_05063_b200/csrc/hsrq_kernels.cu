@@ -497,8 +497,16 @@ struct HostFeed {
   int64_t ldh_host;
   double* X_host;        // solution destination (column-major, ldx_host), or null
   int64_t ldx_host;
-  cudaStream_t copy;     // copy stream (also runs the per-block table kernels)
+  cudaStream_t copy;     // H2D copy stream (also runs the per-block table kernels)
   cudaEvent_t* blk;      // N + 2 events: blk[b] = block b copied and tabulated; blk[N + 1] entry
+  cudaStream_t d2h;      // D2H stream for X (its own copy engine: overlaps the next H2D)
+  int wait_on_stream;    // 1: `stream` waits for X on the host at the end (synchronous entry)
+  int early;             // 1: the copy stream starts at once (async entry: the caller
+                         // guarantees the workspace is idle), else after prior work on `stream`
+  int chunks;            // backtransform / X download chunks: a chunk below one wave of
+                         // warps costs a full per-warp latency (~4.5 ms at n = 16000), so
+                         // 4 for the synchronous entry (D2H of chunk c behind chunk c+1)
+                         // and 1 for the async one (the next solve hides the download)
 };
 
 int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const double* lam_re,
@@ -612,8 +620,10 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     // `stream` released the buffers); each block's table kernel follows its
     // copy there, off the sweep's critical path
     cudaStream_t cp = feed->copy;
-    cudaEventRecord(feed->blk[c.N + 1], stream);
-    cudaStreamWaitEvent(cp, feed->blk[c.N + 1], 0);
+    if (!feed->early) {
+      cudaEventRecord(feed->blk[c.N + 1], stream);
+      cudaStreamWaitEvent(cp, feed->blk[c.N + 1], 0);
+    }
     if (!ck(cudaMemsetAsync(c.HM0, 0, sizeof(double) * (size_t)c.N * c.N, cp), "memset") ||
         !ck(cudaMemsetAsync(c.RS, 0, sizeof(double) * (size_t)c.N * c.N, cp), "memset"))
       return HSRQ_ERR_CUDA;
@@ -812,7 +822,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   } else {
     // host feed: backtransform in shift chunks; each chunk's columns of X go
     // to the host on the copy stream while the next chunk is transformed
-    const int nch = 8;
+    const int nch = feed->chunks;
     for (int ch = 0; ch < nch; ch++) {
       const int64_t q0 = c.ms * ch / nch, q1 = c.ms * (ch + 1) / nch;
       if (q1 <= q0) continue;
@@ -822,14 +832,14 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
       // (the block events are free again: every wait on them is already enqueued)
       cudaEvent_t e = feed->blk[ch % (c.N + 1)];
       cudaEventRecord(e, stream);
-      cudaStreamWaitEvent(feed->copy, e, 0);
+      cudaStreamWaitEvent(feed->d2h, e, 0);
       // columns of shifts [q0, q1): complex part then real part
       const int64_t cq1 = std::min<int64_t>(q1, c.mc), rq0 = std::max<int64_t>(q0, c.mc);
       if (cq1 > q0 &&
           !ck(cudaMemcpy2DAsync(feed->X_host + 2 * q0 * feed->ldx_host,
                                 sizeof(double) * feed->ldx_host, c.X + 2 * q0 * c.ldx,
                                 sizeof(double) * c.ldx, sizeof(double) * n,
-                                (size_t)(2 * (cq1 - q0)), cudaMemcpyDeviceToHost, feed->copy),
+                                (size_t)(2 * (cq1 - q0)), cudaMemcpyDeviceToHost, feed->d2h),
               "D2H X"))
         return HSRQ_ERR_CUDA;
       if (q1 > rq0 &&
@@ -837,12 +847,14 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
                                 sizeof(double) * feed->ldx_host,
                                 c.X + (2 * c.mc + rq0 - c.mc) * c.ldx, sizeof(double) * c.ldx,
                                 sizeof(double) * n, (size_t)(q1 - rq0), cudaMemcpyDeviceToHost,
-                                feed->copy),
+                                feed->d2h),
               "D2H X"))
         return HSRQ_ERR_CUDA;
     }
-    cudaEventRecord(feed->blk[c.N + 1], feed->copy);
-    cudaStreamWaitEvent(stream, feed->blk[c.N + 1], 0);  // X is on the host
+    if (feed->wait_on_stream) {
+      cudaEventRecord(feed->blk[c.N + 1], feed->d2h);
+      cudaStreamWaitEvent(stream, feed->blk[c.N + 1], 0);  // X is on the host
+    }
   }
   if (g_timing) {
     // read back lazily (hsrq_phase_times): no host sync inside a timed solve
@@ -970,12 +982,25 @@ size_t hsrq_host_workspace_bytes(int64_t n, int32_t b_r, int64_t m_cplx, int64_t
   return host_layout(n, b_r, m_cplx, m_real).total;
 }
 
-int64_t hsrq_solve_group_host(const double* H, int64_t ldh, int64_t n, int32_t b_r,
-                              const double* lam_re, const double* lam_im, int64_t m_cplx,
-                              int64_t m_real, const double* B, int64_t ldb, int32_t b_broadcast,
-                              double* X, int64_t ldx, int32_t* seg_exp, int32_t* alpha_exp,
-                              double* norms, double* log2norm, int64_t* fail, int32_t robust,
-                              int32_t mode, void* dev_ws, size_t dev_ws_bytes, void* stream_) {
+namespace {
+// Tickets of asynchronous host-buffer solves: the event after the last D2H of
+// the solve, and where its per-shift failure codes land.
+struct HostTicket {
+  cudaEvent_t done = nullptr;
+  const int64_t* fail = nullptr;
+  int64_t ms = 0;
+  int live = 0;
+};
+constexpr int NTICKET = 16;
+thread_local HostTicket g_tickets[NTICKET];
+thread_local int64_t g_ticket_seq = 0;
+
+int64_t host_enqueue(const double* H, int64_t ldh, int64_t n, int32_t b_r, const double* lam_re,
+                     const double* lam_im, int64_t m_cplx, int64_t m_real, const double* B,
+                     int64_t ldb, int32_t b_broadcast, double* X, int64_t ldx, int32_t* seg_exp,
+                     int32_t* alpha_exp, double* norms, double* log2norm, int64_t* fail,
+                     int32_t robust, int32_t mode, void* dev_ws, size_t dev_ws_bytes,
+                     cudaStream_t stream, int early) {
   if (n < 1 || b_r < 1 || b_r > MAXK || b_r > n || m_cplx < 0 || m_real < 0 ||
       m_cplx + m_real < 1 || ldh < n || ldx < n || (!b_broadcast && ldb < n)) {
     snprintf(g_err, sizeof(g_err), "bad configuration (n=%lld b_r=%d)", (long long)n, b_r);
@@ -983,19 +1008,19 @@ int64_t hsrq_solve_group_host(const double* H, int64_t ldh, int64_t n, int32_t b
   }
   const HostLayout L = host_layout(n, b_r, m_cplx, m_real);
   if (dev_ws_bytes < L.total) return HSRQ_ERR_WORKSPACE;
-  cudaStream_t stream = (cudaStream_t)stream_;
   unsigned char* w = (unsigned char*)dev_ws;
   double* Hd = (double*)(w + L.h);
   double* Xd = (double*)(w + L.x);
   const int64_t ms = m_cplx + m_real, ncol = 2 * m_cplx + m_real, N = (n + b_r - 1) / b_r;
-  // per-thread copy stream and event pool (N + 2 events)
-  thread_local cudaStream_t copy = nullptr;
+  // per-thread copy streams (H2D, D2H: separate copy engines) and event pool
+  thread_local cudaStream_t copy = nullptr, d2h = nullptr;
   thread_local int copy_dev = -1;
   thread_local std::vector<cudaEvent_t> evs;
   int dev = 0;
   cudaGetDevice(&dev);
   if (copy_dev != dev) {
-    if (!ck(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "copy stream"))
+    if (!ck(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "copy stream") ||
+        !ck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "d2h stream"))
       return HSRQ_ERR_CUDA;
     for (auto e : evs) cudaEventDestroy(e);
     evs.clear();
@@ -1035,7 +1060,7 @@ int64_t hsrq_solve_group_host(const double* H, int64_t ldh, int64_t n, int32_t b
     Bd = Xd;
     ldbd = n;
   }
-  HostFeed feed{H, ldh, X, ldx, copy, evs.data()};
+  HostFeed feed{H, ldh, X, ldx, copy, evs.data(), d2h, 0, early, early ? 1 : 4};
   int32_t* segd = (int32_t*)(w + L.seg);
   int32_t* aexpd = (int32_t*)(w + L.aexp);
   double* normsd = (double*)(w + L.norms);
@@ -1047,24 +1072,65 @@ int64_t hsrq_solve_group_host(const double* H, int64_t ldh, int64_t n, int32_t b
                                (double*)(w + L.s), n, segd, aexpd, normsd, l2d, faild, robust, mode,
                                wsd, ws_layout(n, b_r, m_cplx, m_real).total, stream, &feed);
   if (r < 0) return r;
-  unsigned long long nf = 0;
-  const WsLayout WL = ws_layout(n, b_r, m_cplx, m_real);
-  if (!ck(cudaMemcpyAsync(seg_exp, segd, sizeof(int32_t) * N * ms, cudaMemcpyDeviceToHost, stream),
-          "D2H seg") ||
-      !ck(cudaMemcpyAsync(alpha_exp, aexpd, sizeof(int32_t) * ms, cudaMemcpyDeviceToHost, stream),
-          "D2H alpha") ||
-      !ck(cudaMemcpyAsync(norms, normsd, sizeof(double) * ms, cudaMemcpyDeviceToHost, stream),
-          "D2H norms") ||
-      !ck(cudaMemcpyAsync(log2norm, l2d, sizeof(double) * ms, cudaMemcpyDeviceToHost, stream),
-          "D2H log2norm") ||
-      !ck(cudaMemcpyAsync(fail, faild, sizeof(int64_t) * ms, cudaMemcpyDeviceToHost, stream),
-          "D2H fail") ||
-      !ck(cudaMemcpyAsync(&nf, (unsigned char*)wsd + WL.nfail, sizeof(nf), cudaMemcpyDeviceToHost,
-                          stream),
-          "D2H nfail") ||
-      !ck(cudaStreamSynchronize(stream), "sync"))
+  // the small per-shift outputs follow X on the D2H stream, after the sweep
+  HostTicket& t = g_tickets[g_ticket_seq % NTICKET];
+  if (t.live) cudaEventSynchronize(t.done);  // ring slot reuse: that solve is long done
+  if (!t.done && !ck(cudaEventCreateWithFlags(&t.done, cudaEventDisableTiming), "ticket event"))
     return HSRQ_ERR_CUDA;
-  return (int64_t)nf;
+  cudaEvent_t swept = evs[N + 1];
+  cudaEventRecord(swept, stream);
+  cudaStreamWaitEvent(d2h, swept, 0);
+  if (!ck(cudaMemcpyAsync(seg_exp, segd, sizeof(int32_t) * N * ms, cudaMemcpyDeviceToHost, d2h),
+          "D2H seg") ||
+      !ck(cudaMemcpyAsync(alpha_exp, aexpd, sizeof(int32_t) * ms, cudaMemcpyDeviceToHost, d2h),
+          "D2H alpha") ||
+      !ck(cudaMemcpyAsync(norms, normsd, sizeof(double) * ms, cudaMemcpyDeviceToHost, d2h),
+          "D2H norms") ||
+      !ck(cudaMemcpyAsync(log2norm, l2d, sizeof(double) * ms, cudaMemcpyDeviceToHost, d2h),
+          "D2H log2norm") ||
+      !ck(cudaMemcpyAsync(fail, faild, sizeof(int64_t) * ms, cudaMemcpyDeviceToHost, d2h),
+          "D2H fail"))
+    return HSRQ_ERR_CUDA;
+  cudaEventRecord(t.done, d2h);
+  t.fail = fail;
+  t.ms = ms;
+  t.live = 1;
+  return g_ticket_seq++;
+}
+}  // namespace
+
+int64_t hsrq_host_wait(int64_t ticket) {
+  if (ticket < 0 || ticket >= g_ticket_seq || ticket < g_ticket_seq - NTICKET) return HSRQ_ERR_CONFIG;
+  HostTicket& t = g_tickets[ticket % NTICKET];
+  if (!ck(cudaEventSynchronize(t.done), "wait")) return HSRQ_ERR_CUDA;
+  int64_t nf = 0;
+  for (int64_t q = 0; q < t.ms; q++) nf += t.fail[q] != 0;
+  return nf;
+}
+
+int64_t hsrq_solve_group_host_async(const double* H, int64_t ldh, int64_t n, int32_t b_r,
+                                    const double* lam_re, const double* lam_im, int64_t m_cplx,
+                                    int64_t m_real, const double* B, int64_t ldb,
+                                    int32_t b_broadcast, double* X, int64_t ldx, int32_t* seg_exp,
+                                    int32_t* alpha_exp, double* norms, double* log2norm,
+                                    int64_t* fail, int32_t robust, int32_t mode, void* dev_ws,
+                                    size_t dev_ws_bytes, void* stream) {
+  return host_enqueue(H, ldh, n, b_r, lam_re, lam_im, m_cplx, m_real, B, ldb, b_broadcast, X, ldx,
+                      seg_exp, alpha_exp, norms, log2norm, fail, robust, mode, dev_ws,
+                      dev_ws_bytes, (cudaStream_t)stream, 1);
+}
+
+int64_t hsrq_solve_group_host(const double* H, int64_t ldh, int64_t n, int32_t b_r,
+                              const double* lam_re, const double* lam_im, int64_t m_cplx,
+                              int64_t m_real, const double* B, int64_t ldb, int32_t b_broadcast,
+                              double* X, int64_t ldx, int32_t* seg_exp, int32_t* alpha_exp,
+                              double* norms, double* log2norm, int64_t* fail, int32_t robust,
+                              int32_t mode, void* dev_ws, size_t dev_ws_bytes, void* stream) {
+  const int64_t t = host_enqueue(H, ldh, n, b_r, lam_re, lam_im, m_cplx, m_real, B, ldb,
+                                 b_broadcast, X, ldx, seg_exp, alpha_exp, norms, log2norm, fail,
+                                 robust, mode, dev_ws, dev_ws_bytes, (cudaStream_t)stream, 0);
+  if (t < 0) return t;
+  return hsrq_host_wait(t);
 }
 
 int64_t hsrq_last_launch_count(void) { return g_launches; }

@@ -246,22 +246,35 @@ class HostGroupSolver:
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
 
     def launch(self, h, lam_re, lam_im, b, broadcast, out, robust=True, mode="eigvec",
-               stream=None):
+               stream=None, wait=True):
         """h: (n, n) float64 column-major (Fortran) array; lam_*: (ms,) complex-first;
-        b: (n,) start vector (broadcast) or (ncol, n) rows = columns; out: HostOutput."""
+        b: (n,) start vector (broadcast) or (ncol, n) rows = columns; out: HostOutput.
+        ``wait=False`` enqueues only (hsrq_solve_group_host_async) and returns the
+        ticket for ``wait_ticket``; the host buffers must stay alive until then."""
         h = np.asarray(h)
         if not (h.flags.f_contiguous and h.dtype == np.float64):
             h = np.asfortranarray(h, dtype=np.float64)
         stream = stream or torch.cuda.current_stream(self.device)
         P = lambda a: ctypes.c_void_p(a.ctypes.data) if a is not None else ctypes.c_void_p(0)
         mode_i = {"solve": 0, "eigvec": 1}[mode]
-        r = self.lib.hsrq_solve_group_host(
+        fn = self.lib.hsrq_solve_group_host if wait else self.lib.hsrq_solve_group_host_async
+        r = fn(
             P(h), h.shape[0], self.n, self.b_r, P(lam_re), P(lam_im), self.mc, self.mr, P(b),
             0 if broadcast else self.n, 1 if broadcast else 0, P(out.X), self.n, P(out.seg_exp),
             P(out.alpha_exp), P(out.norms), P(out.log2norm), P(out.fail), int(bool(robust)),
             mode_i, _ptr(self.ws), self.ws_bytes, ctypes.c_void_p(stream.cuda_stream))
         if r < 0:
             raise RuntimeError(f"hsrq_solve_group_host failed ({r}): {_lib.last_error()}")
+        if not wait:
+            return int(r)
+        out.nfail = int(r)
+        return out
+
+    def wait_ticket(self, ticket, out):
+        """Complete an asynchronous launch: outputs on the host, ``out.nfail`` set."""
+        r = self.lib.hsrq_host_wait(int(ticket))
+        if r < 0:
+            raise RuntimeError(f"hsrq_host_wait failed ({r}): {_lib.last_error()}")
         out.nfail = int(r)
         return out
 

@@ -53,3 +53,41 @@ def test_host_entry_matches_device_entry(dev, n, b_r, seed, kind, robust, mode):
     assert np.array_equal(hout.norms, dout.norms.cpu().numpy(), equal_nan=True)
     assert np.array_equal(hout.log2norm, dout.log2norm.cpu().numpy(), equal_nan=True)
     assert np.array_equal(hout.fail, dout.fail.cpu().numpy())
+
+
+def test_async_host_entry_two_in_flight(dev):
+    """hsrq_solve_group_host_async: three different solve groups enqueued
+    back to back on two workspaces (the third reuses the first after waiting)
+    give exactly the synchronous entry's results."""
+    import instances
+    from paper_2101_05063_b200.solver import HostGroupSolver
+
+    n, b_r = 700, 128
+    h = np.asfortranarray(instances.random_hessenberg(n, 9))
+    ev = np.linalg.eigvals(h)
+    groups = []
+    for off in (0.0, 0.25, 0.5):
+        er = ev[ev.imag == 0].real[:4] + off
+        ec = ev[ev.imag > 0][:5] + 1j * off
+        lam = np.concatenate([ec, er.astype(np.complex128)])
+        groups.append((np.ascontiguousarray(lam.real), np.ascontiguousarray(lam.imag)))
+    b = np.full(n, 1e-3)
+    solvers = [HostGroupSolver(n, b_r, 5, 4, dev), HostGroupSolver(n, b_r, 5, 4, dev)]
+    want = []
+    for lre, lim in groups:
+        o = solvers[0].new_output()
+        want.append(solvers[0].launch(h, lre, lim, b, True, o))
+    outs = [solvers[0].new_output(pinned=True), solvers[1].new_output(pinned=True)]
+    got = []
+    t0 = solvers[0].launch(h, *groups[0], b, True, outs[0], wait=False)
+    t1 = solvers[1].launch(h, *groups[1], b, True, outs[1], wait=False)
+    solvers[0].wait_ticket(t0, outs[0])
+    got.append((outs[0].X.copy(), outs[0].seg_exp.copy(), outs[0].nfail))
+    t2 = solvers[0].launch(h, *groups[2], b, True, outs[0], wait=False)
+    solvers[1].wait_ticket(t1, outs[1])
+    got.append((outs[1].X.copy(), outs[1].seg_exp.copy(), outs[1].nfail))
+    solvers[0].wait_ticket(t2, outs[0])
+    got.append((outs[0].X.copy(), outs[0].seg_exp.copy(), outs[0].nfail))
+    for w, (x, seg, nf) in zip(want, got):
+        assert nf == w.nfail
+        assert np.array_equal(x, w.X) and np.array_equal(seg, w.seg_exp)

@@ -6,6 +6,7 @@ import subprocess
 exec(open("tools/profile_solve.py").read().split("import ctypes")[0])
 from paper_2101_05063_b200 import _lib
 L = _lib.load()
+gs.launch(start, True)  # one solve with the timeline armed (HSRQ_TIMELINE = tile column)
 L.hsrq_debug_timeline.restype = ctypes.c_int64
 buf = np.zeros(8192 * 8, dtype=np.uint64)
 print("rc", L.hsrq_debug_timeline(ctypes.c_void_p(buf.ctypes.data)))
