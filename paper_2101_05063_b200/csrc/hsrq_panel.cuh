@@ -435,9 +435,18 @@ __device__ __forceinline__ void seg_max2(PanelSmem& sm, int slot, int sg, int cl
 // every CTA holds one full tile row, so there is one guard segment, no row is
 // masked, and all per-column scalars are hoisted out of the row loop.  The
 // arithmetic is exactly that of the general epilogue in panel_body.
+__device__ __forceinline__ void tl_mark(unsigned long long* tlp, int slot) {
+  if (tlp) {  // diagnostics (HSRQ_TIMELINE): globaltimer at an epilogue phase mark
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    tlp[slot] = g;
+  }
+}
+
 __device__ __forceinline__ void epilogue_b128(const Ctx& c, const PanelArgs& p, PanelSmem& sm,
                                               const int tid, const int tile0,
-                                              const int64_t col0) {
+                                              const int64_t col0,
+                                              unsigned long long* tlp = nullptr) {
   const int pc = tid / EP_ROWS, rp = tid % EP_ROWS;
   const int cl0 = 2 * pc;
   const int64_t gc0 = col0 + cl0;
@@ -470,6 +479,7 @@ __device__ __forceinline__ void epilogue_b128(const Ctx& c, const PanelArgs& p, 
   const double pz0 = s0.fx * s0.x2, pz1 = s1.fx * s1.x2;
   const double* Z0 = sm.u.C[2 * cl0 + 1];
   const double* Z1 = sm.u.C[2 * cl0 + 3];
+  tl_mark(tlp, 5);
   // ---- pass 1: X'' and the step-3 maxima ----
   double mb0 = 0.0, mb1 = 0.0, mr0 = 0.0, mr1 = 0.0;
   if (cplx) {
@@ -539,6 +549,7 @@ __device__ __forceinline__ void epilogue_b128(const Ctx& c, const PanelArgs& p, 
     sm.red[1][0][cl0] = dkey(mr0);
     sm.red[1][0][cl0 + 1] = dkey(mr1);
   }
+  tl_mark(tlp, 6);
   __syncthreads();
   // ---- step 3 guard (:287-301), one thread per column ----
   int my_need = 0;
@@ -608,6 +619,7 @@ __device__ __forceinline__ void epilogue_b128(const Ctx& c, const PanelArgs& p, 
     }
     __syncthreads();
   }
+  tl_mark(tlp, 7);
   // ---- pass 2: X''' = x3 X'' - Cr_old zk ; Cr_new = A W + P Cr_old - c0 lambda e_{js-1} ----
   const double* W0 = sm.u.C[2 * cl0];
   const double* W1 = sm.u.C[2 * cl0 + 2];
@@ -689,6 +701,7 @@ __device__ __forceinline__ void epilogue_b128(const Ctx& c, const PanelArgs& p, 
       c.XB[ix1] = mb1;
     }
   }
+  tl_mark(tlp, 4);
 }
 
 template <bool A16, bool SEG16, bool FAST>
@@ -834,7 +847,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
   __syncthreads();
 
   if (FAST) {  // b_r == 128: one full tile row per CTA, a single guard segment
-    epilogue_b128(c, p, sm, tid, tile0, col0);
+    epilogue_b128(c, p, sm, tid, tile0, col0, tl_ ? tlp_ : nullptr);
     return;
   }
   // ---------------- epilogue ----------------
