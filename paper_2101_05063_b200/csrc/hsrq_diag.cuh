@@ -67,10 +67,21 @@ __device__ __forceinline__ double hget(const Ctx& c, const DiagArgs& a, int i, i
 // while the current step runs.
 __device__ __forceinline__ void fill_col(const Ctx& c, const DiagArgs& a, double* buf, int t,
                                          int nrows, int lane) {
-  for (int i = lane; i < nrows; i += 32) {
-    const double* src = a.tile_mode ? &a.t_hdiag[(int64_t)i * (a.k - 1) + t]
-                                    : &c.H[(a.js + t) * c.ldh + a.js + i];
-    cp_async8(&buf[i], src, true);
+  if (!a.tile_mode && ((c.ldh | a.js) & 1) == 0) {
+    // contiguous, 16-byte aligned column segment: two rows per cp.async
+    const double* src = c.H + (a.js + t) * c.ldh + a.js;
+    for (int i = 2 * lane; i < nrows; i += 64) {
+      if (i + 1 < nrows)
+        cp_async16(&buf[i], src + i, true);
+      else
+        cp_async8(&buf[i], src + i, true);
+    }
+  } else {
+    for (int i = lane; i < nrows; i += 32) {
+      const double* src = a.tile_mode ? &a.t_hdiag[(int64_t)i * (a.k - 1) + t]
+                                      : &c.H[(a.js + t) * c.ldh + a.js + i];
+      cp_async8(&buf[i], src, true);
+    }
   }
   cp_commit();
 }

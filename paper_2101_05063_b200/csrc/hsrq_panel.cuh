@@ -435,13 +435,20 @@ __device__ __forceinline__ void seg_max2(PanelSmem& sm, int slot, int sg, int cl
 // every CTA holds one full tile row, so there is one guard segment, no row is
 // masked, and all per-column scalars are hoisted out of the row loop.  The
 // arithmetic is exactly that of the general epilogue in panel_body.
+// Diagnostics: compile with -DHSRQ_TIMELINE_EPI to time the fast epilogue's
+// phases (HSRQ_TIMELINE=jt; tools/debug/timeline.py).  Off by default: the
+// extra live pointer perturbs k_panel's register allocation (336 -> 342 ms).
+#ifdef HSRQ_TIMELINE_EPI
 __device__ __forceinline__ void tl_mark(unsigned long long* tlp, int slot) {
-  if (tlp) {  // diagnostics (HSRQ_TIMELINE): globaltimer at an epilogue phase mark
+  if (tlp) {
     unsigned long long g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
     tlp[slot] = g;
   }
 }
+#else
+__device__ __forceinline__ void tl_mark(unsigned long long*, int) {}
+#endif
 
 __device__ __forceinline__ void epilogue_b128(const Ctx& c, const PanelArgs& p, PanelSmem& sm,
                                               const int tid, const int tile0,
@@ -847,7 +854,11 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
   __syncthreads();
 
   if (FAST) {  // b_r == 128: one full tile row per CTA, a single guard segment
+#ifdef HSRQ_TIMELINE_EPI
     epilogue_b128(c, p, sm, tid, tile0, col0, tl_ ? tlp_ : nullptr);
+#else
+    epilogue_b128(c, p, sm, tid, tile0, col0);
+#endif
     return;
   }
   // ---------------- epilogue ----------------
