@@ -731,16 +731,18 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
       cd.ldc = KP;
       a.rot_off = 0;
     }
-    if (mr > 0) {
-      a.q0 = mc;
-      a.count = mr;
-      diag_launch(false, cd, a, fork ? sside : sd);
-      g_launches++;
-    }
+    // complex first: its sweep is the longer one (the critical path), so its
+    // CTAs should be resident before the real kernel's fill the rest
     if (mc > 0) {
       a.q0 = 0;
       a.count = mc;
       diag_launch(true, cd, a, sd);
+      g_launches++;
+    }
+    if (mr > 0) {
+      a.q0 = mc;
+      a.count = mr;
+      diag_launch(false, cd, a, fork ? sside : sd);
       g_launches++;
     }
     if (fork) {
