@@ -69,3 +69,38 @@ def test_bench_csv_rows(tmp_path):
         assert r["schema"] == "hessrq-bench-v1" and r["backend"] == "b200"
         assert float(r["total_s"]) > 0 and float(r["henry_s"]) > 0
         assert float(r["gpu_panel_s"]) > 0 and float(r["flops_Update"]) > 0
+
+
+def test_henry_config3_sample_bitwise(oracle):
+    """Config-3-sized sweep (n = 4000, random Hessenberg as in the BASELINE
+    complex-shift config) on a sample of eigenvalue shifts: GPU == oracle bit
+    for bit, real and complex (inf / NaN positions included).  Where the
+    unguarded single sweep stays finite the result is an eigenvector
+    direction; where it overflows -- the failure the paper's scaling exists
+    for -- the robust tiled solve of the same shift is finite."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "tools"))
+    import instances
+    from paper_2101_05063_b200 import chsrq3, dhsrq3, henry_rq_solve
+
+    h = instances.make_h(3)
+    ev = np.load(instances.eig_path(3))
+    n = h.shape[0]
+    for lam in (ev[ev.imag == 0].real[:4], ev[ev.imag > 0][:4]):
+        b = np.ones((n, lam.size)) + (0j if np.iscomplexobj(lam) else 0)
+        st, want = oracle.henry_solve(h, lam, b)
+        assert st == 0
+        x = henry_rq_solve(h, lam, b)
+        np.testing.assert_array_equal(x, want)
+        hf = np.linalg.norm(h, "fro")
+        robust = (chsrq3 if np.iscomplexobj(lam) else dhsrq3)(h, lam, b, mode="eigvec")
+        for l in range(lam.size):
+            if np.all(np.isfinite(x[:, l])):
+                xl = x[:, l] / np.linalg.norm(x[:, l])
+            else:
+                xl = robust.x[:, l]
+                assert np.all(np.isfinite(xl))
+            assert np.linalg.norm(h @ xl - lam[l] * xl) / hf <= 10 * n * np.finfo(float).eps
