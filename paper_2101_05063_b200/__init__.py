@@ -11,6 +11,7 @@ from .core import (
     ConfigError,
     HessenbergMatrix,
     HessrqError,
+    RunStats,
     ScalingMatrix,
     SingularSystemError,
     SolutionBlock,

@@ -7,6 +7,8 @@ or, with ``robust=False``, the unguarded tiled solve.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from .core import ConfigError, SolutionBlock, as_hessenberg
@@ -21,6 +23,35 @@ def _driver(h, shifts, b, kind, *, b_r=None, b_c=32, workers=1, robust=True, mod
     n = h.n
     if b_r is None:
         b_r = min(MAX_TILE, n)
+    lib = None
+    if stats is not None:  # per-phase device times for the RunStats counters
+        from . import _lib
+
+        lib = _lib.load()
+        lib.hsrq_phase_times((ctypes.c_double * 5)())  # drop stale timings
+        lib.hsrq_set_timing(1)
+    try:
+        out, m, cplx = _run(h, shifts, b, kind, n, b_r, b_c, robust, mode, device,
+                            compact_rotations)
+    finally:
+        if lib is not None:
+            lib.hsrq_set_timing(0)
+    if stats is not None:
+        from . import flops
+        from .benchcsv import GPU_PHASES, task_seconds
+
+        ph = (ctypes.c_double * 5)()
+        lib.hsrq_phase_times(ph)
+        ex, fo = flops.task_flops(n, b_r, m, cplx)
+        sec = task_seconds(dict(zip(GPU_PHASES, [v / 1e3 for v in ph])), ex)
+        for t in flops.TASK_TYPES:
+            stats.add(t, sec[t], ex[t], fo[t])
+    if out.nfail:
+        raise_first_failure(out.fail.cpu().numpy(), b_c, [(0, m)])
+    return to_solution_block(out, n, robust=robust, want_cplx=cplx)
+
+
+def _run(h, shifts, b, kind, n, b_r, b_c, robust, mode, device, compact_rotations):
     if kind == "complex":
         lam = np.asarray(shifts, dtype=np.complex128).ravel()
         m = lam.size
@@ -36,9 +67,7 @@ def _driver(h, shifts, b, kind, *, b_r=None, b_c=32, workers=1, robust=True, mod
         B = np.ascontiguousarray(np.asarray(b, dtype=np.float64).reshape(n, m).T)
         out, _ = solve_group(h, None, lam, B, b_r, robust=robust, mode=mode, b_c=b_c,
                              device=device, compact=compact_rotations)
-    if out.nfail:
-        raise_first_failure(out.fail.cpu().numpy(), b_c, [(0, m)])
-    return to_solution_block(out, n, robust=robust, want_cplx=(kind == "complex"))
+    return out, m, kind == "complex"
 
 
 def dhsrq3(h, shifts, b, **kw) -> SolutionBlock:

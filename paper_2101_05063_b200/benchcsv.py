@@ -110,6 +110,22 @@ def gen_shifts(h, count, kind, seed=2, radius=1.5):
     raise ConfigError(f"unknown shift kind {kind!r}")
 
 
+def task_seconds(gpu, ex):
+    """Per-task-type seconds from the fused kernels' measured times (``gpu``:
+    phase -> s) split in proportion to the exact flop counts ``ex``:
+    ReduceDiag + Solve share the diagonal sweeps, ReduceOffdiag + Update the
+    panel GEMM and guard-scalar kernels; Backtransform is its own kernel."""
+    sec = {}
+    d = ex["ReduceDiag"] + ex["Solve"]
+    for t in ("ReduceDiag", "Solve"):
+        sec[t] = gpu["diag"] * ex[t] / d if d else 0.0
+    o = ex["ReduceOffdiag"] + ex["Update"]
+    for t in ("ReduceOffdiag", "Update"):
+        sec[t] = (gpu["panel"] + gpu["scalars"]) * ex[t] / o if o else 0.0
+    sec["Backtransform"] = gpu["backtransform"]
+    return sec
+
+
 def header():
     return (["schema", "backend", "n", "m", "kind", "b_r", "b_c", "workers", "robust"]
             + list(TASK_TYPES) + ["total_s"] + [f"flops_{t}" for t in TASK_TYPES]
@@ -136,6 +152,7 @@ def bench_rows(h, shifts, rhs, tile_rows=128, batch=32, robust_modes=(True,),
         t0 = time.perf_counter()
         fn(h, shifts, rhs, b_r=b_r, b_c=batch, robust=robust)
         total = time.perf_counter() - t0
+        lib.hsrq_phase_times(np.zeros(5).ctypes.data)  # drop any stale timings
         lib.hsrq_set_timing(1)
         try:
             fn(h, shifts, rhs, b_r=b_r, b_c=batch, robust=robust)
@@ -144,14 +161,7 @@ def bench_rows(h, shifts, rhs, tile_rows=128, batch=32, robust_modes=(True,),
         finally:
             lib.hsrq_set_timing(0)
         gpu = dict(zip(GPU_PHASES, ph / 1e3))
-        sec = {}
-        d = ex["ReduceDiag"] + ex["Solve"]
-        for t in ("ReduceDiag", "Solve"):
-            sec[t] = gpu["diag"] * ex[t] / d if d else 0.0
-        o = ex["ReduceOffdiag"] + ex["Update"]
-        for t in ("ReduceOffdiag", "Update"):
-            sec[t] = (gpu["panel"] + gpu["scalars"]) * ex[t] / o if o else 0.0
-        sec["Backtransform"] = gpu["backtransform"]
+        sec = task_seconds(gpu, ex)
         henry_s = ""
         if compare_henry:
             henry_rq_solve(h, shifts, rhs)  # warm-up

@@ -116,3 +116,22 @@ class SolutionBlock:
     flops: dict = field(default_factory=dict)
     alpha_exp: np.ndarray | None = None
     log2_norms: np.ndarray | None = None
+
+
+class RunStats:
+    """Per-task-type time and flop accumulators (scheduler.py:98-119): the
+    ``stats`` argument of dhsrq3 / chsrq3.  The B200 kernels fuse task types,
+    so a solve adds each type once, with the measured fused-kernel time split
+    in proportion to the reference flop model (see benchcsv.task_seconds)."""
+
+    def __init__(self):
+        self.seconds = {}
+        self.flops = {}
+        self.formula = {}
+        self.calls = {}
+
+    def add(self, task_type, seconds, flops=0.0, formula=0.0):
+        self.seconds[task_type] = self.seconds.get(task_type, 0.0) + seconds
+        self.flops[task_type] = self.flops.get(task_type, 0.0) + flops
+        self.formula[task_type] = self.formula.get(task_type, 0.0) + formula
+        self.calls[task_type] = self.calls.get(task_type, 0) + 1

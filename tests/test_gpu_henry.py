@@ -104,3 +104,23 @@ def test_henry_config3_sample_bitwise(oracle):
                 xl = robust.x[:, l]
                 assert np.all(np.isfinite(xl))
             assert np.linalg.norm(h @ xl - lam[l] * xl) / hf <= 10 * n * np.finfo(float).eps
+
+
+def test_dhsrq3_fills_runstats():
+    """dhsrq3 / chsrq3 ``stats``: the reference's RunStats fields, exact flop
+    and formula counters (= the reference's, tests/golden/runstats.npz via
+    flops.task_flops), measured per-task seconds."""
+    from paper_2101_05063_b200 import RunStats, chsrq3, dhsrq3, flops
+
+    rng = np.random.default_rng(3)
+    n = 300
+    h = np.triu(rng.standard_normal((n, n)))
+    h[np.arange(1, n), np.arange(n - 1)] = np.abs(rng.standard_normal(n - 1)) + 0.1
+    for cplx in (False, True):
+        lam = rng.uniform(2, 3, 5) + (0.5j if cplx else 0)
+        b = np.ones((n, 5)) + (0j if cplx else 0)
+        st = RunStats()
+        (chsrq3 if cplx else dhsrq3)(h, lam, b, b_r=64, stats=st)
+        ex, fo = flops.task_flops(n, 64, 5, cplx)
+        assert st.flops == ex and st.formula == fo
+        assert all(st.seconds[t] > 0 for t in flops.TASK_TYPES)
