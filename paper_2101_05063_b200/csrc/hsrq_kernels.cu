@@ -120,6 +120,23 @@ __device__ __forceinline__ int64_t pack_fail(int phase, int tile, int row) {
 // setup: HM0 / RS tables (per H, b_r), crossover init, X init
 // ---------------------------------------------------------------------------
 
+// atomicMax of non-negative doubles into tile-row slots, warp-reduced first
+// when the warp's 32 rows share one tile (b_r a multiple of 32): one atomic
+// per warp instead of 32 contending on one address (max is order-free).
+__device__ __forceinline__ void tile_max2(double* slot_a, double a, double* slot_b, double b,
+                                          bool warp_uniform) {
+  if (warp_uniform) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if ((threadIdx.x & 31) != 0) return;
+  }
+  atomicMax((unsigned long long*)slot_a, dkey(a));
+  atomicMax((unsigned long long*)slot_b, dkey(b));
+}
+
 // HM0[jt][i] = max_{r in tile i} |H[r, js-1]|             (update_rupdate :207-210)
 // RS[jt][i]  = max_{r in tile i} sum_{j=1}^{k-1} |htile[r, j]| (:256-262),
 // summed left to right like the reference.  One thread per (row, jt).
@@ -128,6 +145,9 @@ __global__ void k_tables(Ctx c) {
   int jt = blockIdx.y + 1;
   if (jt >= c.N) return;
   int64_t js = (int64_t)jt * c.b_r;
+  // js is a multiple of b_r: with b_r % 32 == 0 a warp is wholly inside or
+  // outside the rows < js, and its rows share one tile
+  const bool wu = (c.b_r & 31) == 0 && (blockDim.x & 31) == 0;
   if (r >= js) return;
   int64_t je = js + c.b_r < c.n ? js + c.b_r : c.n;
   int k = (int)(je - js);
@@ -135,8 +155,7 @@ __global__ void k_tables(Ctx c) {
   double h0 = fabs(c.H[(js - 1) * c.ldh + r]);
   double acc = 0.0;
   for (int j = 1; j < k; j++) acc += fabs(c.H[(js - 1 + j) * c.ldh + r]);
-  atomicMax((unsigned long long*)&c.HM0[(int64_t)jt * c.N + i], dkey(h0));
-  atomicMax((unsigned long long*)&c.RS[(int64_t)jt * c.N + i], dkey(acc));
+  tile_max2(&c.HM0[(int64_t)jt * c.N + i], h0, &c.RS[(int64_t)jt * c.N + i], acc, wu);
 }
 
 // HMK[jt][kp] = max_{i<kp} |H[js+i, js+kp-1]| (the hmax of solve_rsolve :155-163).
@@ -174,12 +193,12 @@ __global__ void k_tables_jt(Ctx c, int jt) {
   }
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (jt < 1 || r >= js) return;
+  const bool wu = (c.b_r & 31) == 0 && (blockDim.x & 31) == 0;
   const int i = (int)(r / c.b_r);
   const double h0 = fabs(c.H[(js - 1) * c.ldh + r]);
   double acc = 0.0;
   for (int j = 1; j < k; j++) acc += fabs(c.H[(js - 1 + j) * c.ldh + r]);
-  atomicMax((unsigned long long*)&c.HM0[(int64_t)jt * c.N + i], dkey(h0));
-  atomicMax((unsigned long long*)&c.RS[(int64_t)jt * c.N + i], dkey(acc));
+  tile_max2(&c.HM0[(int64_t)jt * c.N + i], h0, &c.RS[(int64_t)jt * c.N + i], acc, wu);
 }
 
 // X = B (or the broadcast start vector), Cr(:, N-1) = H(:, n-1) - lambda e_n
