@@ -204,22 +204,31 @@ __global__ void k_tables_jt(Ctx c, int jt) {
 // X = B (or the broadcast start vector), Cr(:, N-1) = H(:, n-1) - lambda e_n
 // (reduce.py:66-69, 77-78).
 __global__ void k_init(Ctx c, const double* B, int64_t ldb, int b_broadcast) {
-  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t col = blockIdx.y;
-  if (r >= c.n || col >= c.ncol) return;
-  bool cplx = col < 2 * c.mc;
-  bool im = cplx && (col & 1);
-  int64_t q = cplx ? col / 2 : c.mc + (col - 2 * c.mc);
-  double b = b_broadcast ? (im ? 0.0 : B[r]) : B[col * ldb + r];
-  c.X[col * c.ldx + r] = b;
-  if (!im) {
-    double bb = fabs(b);
-    if (cplx && !b_broadcast) bb = bb + fabs(B[(col + 1) * ldb + r]);
-    atomicMax((unsigned long long*)&c.XB[(r / c.b_r) * c.ms + q], dkey(bb));
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t col = blockIdx.y;
+  const bool valid = r < c.n && col < c.ncol;
+  const bool cplx = col < 2 * c.mc;
+  const bool im = cplx && (col & 1);
+  const int64_t q = cplx ? col / 2 : c.mc + (col - 2 * c.mc);
+  double bb = 0.0;
+  if (valid) {
+    const double b = b_broadcast ? (im ? 0.0 : B[r]) : B[col * ldb + r];
+    c.X[col * c.ldx + r] = b;
+    bb = fabs(b);
+    if (cplx && !im && !b_broadcast) bb = bb + fabs(B[(col + 1) * ldb + r]);
+    double h = im ? 0.0 : c.H[(c.n - 1) * c.ldh + r];
+    if (r == c.n - 1) h -= im ? c.lam_im[q] : c.lam_re[q];
+    c.Cr[col * c.ldx + r] = h;
   }
-  double h = im ? 0.0 : c.H[(c.n - 1) * c.ldh + r];
-  if (r == c.n - 1) h -= im ? c.lam_im[q] : c.lam_re[q];
-  c.Cr[col * c.ldx + r] = h;
+  if (im) return;  // uniform per block (one column per blockIdx.y)
+  // the per-tile bound of max|X| (XB): warp-reduced when a warp's rows share
+  // one tile, one atomic per warp instead of 32 on one address
+  if ((c.b_r & 31) == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bb = fmax(bb, __shfl_xor_sync(0xffffffffu, bb, o));
+    if ((threadIdx.x & 31) != 0) return;
+  }
+  if (valid) atomicMax((unsigned long long*)&c.XB[(r / c.b_r) * c.ms + q], dkey(bb));
 }
 
 __global__ void k_zero_state(Ctx c, int zero_tables) {
