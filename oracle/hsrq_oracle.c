@@ -56,6 +56,12 @@
 #define KIND_SINGULAR 2
 #define EXP_ZERO (-1075) /* exponent of a scale that halved below 2^-1074 */
 
+/* Test hook (oracle_set_stop): end the substitution after tile column jt's
+ * updates, without the backtransform, so intermediate sweep states can be
+ * compared column by column.  -1 = off. */
+static int g_stop_jt = -1;
+void oracle_set_stop(int jt) { g_stop_jt = jt; }
+
 static int64_t pack_status(int64_t kind, int64_t shift, int64_t row) {
     return kind * ((int64_t)1 << 42) + (shift << 21) + row;
 }
@@ -1066,6 +1072,7 @@ static int64_t solve_batch(const double* H, int64_t n, int b_r, int cplx_, int b
 
     /* ---- substitution (backsolve.py:62-313) ---- */
     for (size_t q = 0; q < (size_t)N * b; q++) alpha_e[q] = 0;
+    int stopped = 0;
     for (int jt = N - 1; jt >= 0; jt--) {
         int64_t js = (int64_t)jt * b_r, je = ends[jt];
         int k = (int)(je - js);
@@ -1101,8 +1108,18 @@ static int64_t solve_batch(const double* H, int64_t n, int b_r, int cplx_, int b
                                       s_arr + js * b, alpha_e + (size_t)it * b, X + is * ncol,
                                       robust, omega);
         }
+        if (jt == g_stop_jt) {  /* test hook: the state after column jt's updates */
+            stopped = 1;
+            break;
+        }
     }
-    if (robust) {
+    if (stopped) {
+        for (int l = 0; l < b; l++) {
+            norms[l] = NAN;
+            log2norm[l] = NAN;
+            alpha_col_e[l] = 0;
+        }
+    } else if (robust) {
         if (cplx_)
             oracle_crbacktransform((int)n, b, N, c_re, c_im, s_arr, alpha_e, ends, X, norms,
                                    log2norm, alpha_col_e, mode, omega);

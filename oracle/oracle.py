@@ -314,3 +314,12 @@ def householder_hessenberg(a):
     L.oracle_householder_hessenberg.restype = None
     L.oracle_householder_hessenberg(ctypes.c_int64(n), _p(h), _p(q))
     return h, q
+
+
+def set_stop(jt):
+    """Test hook: oracle solves end after tile column jt's updates (no
+    backtransform; x holds solved tiles >= jt and updated rhs below); -1 off."""
+    L = lib()
+    L.oracle_set_stop.restype = None
+    L.oracle_set_stop.argtypes = [ctypes.c_int]
+    L.oracle_set_stop(int(jt))

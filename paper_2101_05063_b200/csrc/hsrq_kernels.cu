@@ -812,8 +812,14 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     g_launches++;
   };
 
+  // Diagnostics / tests (HSRQ_STOP_AT=s): end the sweep after column s's
+  // panel -- X then holds the solved tiles >= s and the updated right-hand
+  // sides below, E the segment exponents -- without the backtransform.
+  int stop_at = -1;
+  if (const char* e = getenv("HSRQ_STOP_AT")) stop_at = atoi(e);
+  bool stopped = stop_at == c.N - 1 && c.N - 1 == 0;
   run_diag(c.N - 1, stream, side);
-  for (int jt = c.N - 1; jt >= 1; --jt) {
+  for (int jt = c.N - 1; jt >= 1 && !stopped; --jt) {
     PanelArgs p;
     p.jt = jt;
     p.js = (int64_t)jt * b_r;
@@ -828,6 +834,11 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     if (g_timing) {
       cudaEventRecord(tev(jt, 3), stream);
       cudaEventRecord(tev(jt, 4), stream);
+    }
+    if (jt == stop_at) {
+      run_panel(jt, 0, jt);
+      stopped = true;
+      break;
     }
     if (lookahead) {
       run_panel(jt, jt - 1, jt);  // tile row jt-1: all the next sweep needs
@@ -845,7 +856,9 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     }
   }
   if (g_timing) cudaEventRecord(ev[nev - 3], stream);
-  if (!feed || !feed->X_host) {
+  if (stopped) {
+    // (timing of a stopped sweep is not recorded)
+  } else if (!feed || !feed->X_host) {
     k_backtransform<<<(unsigned)((c.ms + BT_WARPS - 1) / BT_WARPS), BT_WARPS * 32, 0, stream>>>(
         c, alpha_exp, norms, log2norm, 0, c.ms);
     g_launches++;
@@ -886,7 +899,10 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
       cudaStreamWaitEvent(stream, feed->blk[c.N + 1], 0);  // X is on the host
     }
   }
-  if (g_timing) {
+  if (g_timing && stopped) {  // a stopped sweep leaves later columns' events unrecorded
+    for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
+    delete[] ev;
+  } else if (g_timing) {
     // read back lazily (hsrq_phase_times): no host sync inside a timed solve
     cudaEventRecord(ev[nev - 2], stream);
     g_pending.push_back(PendingTiming{ev, nev, c.N});
