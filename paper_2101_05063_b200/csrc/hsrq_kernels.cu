@@ -859,8 +859,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   if (stopped) {
     // (timing of a stopped sweep is not recorded)
   } else if (!feed || !feed->X_host) {
-    k_backtransform<<<(unsigned)((c.ms + BT_WARPS - 1) / BT_WARPS), BT_WARPS * 32, 0, stream>>>(
-        c, alpha_exp, norms, log2norm, 0, c.ms);
+    bt_launch(c, alpha_exp, norms, log2norm, 0, c.ms, c.ms, stream);
     g_launches++;
   } else {
     // host feed: backtransform in shift chunks; each chunk's columns of X go
@@ -869,8 +868,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     for (int ch = 0; ch < nch; ch++) {
       const int64_t q0 = c.ms * ch / nch, q1 = c.ms * (ch + 1) / nch;
       if (q1 <= q0) continue;
-      k_backtransform<<<(unsigned)((q1 - q0 + BT_WARPS - 1) / BT_WARPS), BT_WARPS * 32, 0,
-                        stream>>>(c, alpha_exp, norms, log2norm, q0, q1);
+      bt_launch(c, alpha_exp, norms, log2norm, q0, q1, c.ms, stream);
       g_launches++;
       // (the block events are free again: every wait on them is already enqueued)
       cudaEvent_t e = feed->blk[ch % (c.N + 1)];
@@ -1278,8 +1276,7 @@ int64_t hsrq_tile_backtransform(int64_t n, int32_t b_r, int32_t b, int32_t cplx,
       !ck(cudaMemsetAsync(fail, 0, sizeof(int64_t) * b, stream), "memset"))
     return HSRQ_ERR_CUDA;
   c.fail = fail;
-  k_backtransform<<<(unsigned)((b + BT_WARPS - 1) / BT_WARPS), BT_WARPS * 32, 0, stream>>>(
-      c, alpha_exp, norms, l2, 0, b);
+  bt_launch(c, alpha_exp, norms, l2, 0, b, b, stream);
   const bool ok = ck(cudaGetLastError(), "launch");
   cudaFreeAsync(fail, stream);
   cudaFreeAsync(l2, stream);
