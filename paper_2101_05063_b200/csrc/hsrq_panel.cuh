@@ -20,6 +20,10 @@
 // CTA owns whole tile rows, so step 3 -- which needs the GEMM result -- is
 // CTA-local in the epilogue.
 
+#ifndef SCAL_MINB
+#define SCAL_MINB 6  // k_scalars: 6 CTAs per SM (80 registers): 28.7 -> 27.6 ms at config 5
+#endif
+
 struct PanelArgs {
   int jt;
   int64_t js;
@@ -223,7 +227,7 @@ __device__ __forceinline__ void seg_xprime_max(const double* __restrict__ Xr,
 // bound fails does the thread read its b segment for the exact maximum --
 // for complex columns as scaled squared moduli certified on an interval (see
 // k_diag_cplx guard 2), glibc moduli only at a binade edge.
-__global__ void k_scalars(Ctx c, PanelArgs p, RowScalars* RSc) {
+__global__ void __launch_bounds__(128, SCAL_MINB) k_scalars(Ctx c, PanelArgs p, RowScalars* RSc) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int jt = p.jt;
   if (t >= (int64_t)jt * c.ms) return;
