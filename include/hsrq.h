@@ -135,6 +135,27 @@ int64_t hsrq_solve_group_async(const double* H, int64_t ldh, int64_t n, int32_t 
 int64_t hsrq_failure_count(void* ws, void* stream);
 
 /*
+ * CUDA-graph form of one solve group, for callers that repeat a solve of the
+ * same shape on the same buffers (new shifts or right-hand sides written into
+ * lam_re / lam_im / B between launches): hsrq_graph_capture runs the solve
+ * once eagerly, then captures the whole sweep (every kernel, the side-stream
+ * forks and joins) into an executable graph returned in *graph_out;
+ * hsrq_graph_launch replays it on `stream` (one launch instead of ~12 per
+ * tile column -- what matters for small, launch-bound problems); the
+ * failure count is read with hsrq_failure_count(ws, stream).  Timing
+ * (hsrq_set_timing) must be off.  hsrq_graph_destroy frees the graph.
+ */
+int64_t hsrq_graph_capture(const double* H, int64_t ldh, int64_t n, int32_t b_r,
+                           const double* lam_re, const double* lam_im, int64_t m_cplx,
+                           int64_t m_real, const double* B, int64_t ldb, int32_t b_broadcast,
+                           double* X, int64_t ldx, double* c_re, double* c_im, double* s,
+                           int64_t ldc, int32_t* seg_exp, int32_t* alpha_exp, double* norms,
+                           double* log2norm, int64_t* fail, int32_t robust, int32_t mode, void* ws,
+                           size_t ws_bytes, void* stream, void** graph_out);
+int64_t hsrq_graph_launch(void* graph, void* stream);
+void hsrq_graph_destroy(void* graph);
+
+/*
  * Host-buffer variant of hsrq_solve_group -- the calling convention of the
  * reference's _solve_group (numpy arrays in, SolutionBlock arrays out), for
  * a ctypes / FFI binding without any device-array library.  Every pointer is

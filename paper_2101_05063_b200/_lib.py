@@ -34,6 +34,13 @@ SIGNATURES = {
          _p, _p, _p, _p, _p, _i32, _i32, _p, _sz, _p],
     ),
     "hsrq_failure_count": (_i64, [_p, _p]),
+    "hsrq_graph_capture": (
+        _i64,
+        [_p, _i64, _i64, _i32, _p, _p, _i64, _i64, _p, _i64, _i32, _p, _i64, _p, _p, _p, _i64,
+         _p, _p, _p, _p, _p, _i32, _i32, _p, _sz, _p, _p],
+    ),
+    "hsrq_graph_launch": (_i64, [_p, _p]),
+    "hsrq_graph_destroy": (None, [_p]),
     "hsrq_host_workspace_bytes": (_sz, [_i64, _i32, _i64, _i64]),
     "hsrq_solve_group_host": (
         _i64,

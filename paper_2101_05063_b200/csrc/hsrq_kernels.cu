@@ -991,6 +991,58 @@ int64_t hsrq_solve_group_async(const double* H, int64_t ldh, int64_t n, int32_t 
                     ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int64_t hsrq_graph_capture(const double* H, int64_t ldh, int64_t n, int32_t b_r,
+                           const double* lam_re, const double* lam_im, int64_t m_cplx,
+                           int64_t m_real, const double* B, int64_t ldb, int32_t b_broadcast,
+                           double* X, int64_t ldx, double* c_re, double* c_im, double* s,
+                           int64_t ldc, int32_t* seg_exp, int32_t* alpha_exp, double* norms,
+                           double* log2norm, int64_t* fail, int32_t robust, int32_t mode, void* ws,
+                           size_t ws_bytes, void* stream_, void** graph_out) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!graph_out || g_timing) return HSRQ_ERR_CONFIG;
+  // one eager solve first: the per-thread side streams, events and kernel
+  // attributes are created outside the capture
+  int64_t r = solve_impl(H, ldh, n, b_r, lam_re, lam_im, m_cplx, m_real, B, ldb, b_broadcast, X,
+                         ldx, c_re, c_im, s, ldc, seg_exp, alpha_exp, norms, log2norm, fail,
+                         robust, mode, ws, ws_bytes, stream);
+  if (r < 0) return r;
+  // capture on a private stream (the legacy default stream cannot capture)
+  cudaStream_t cap = nullptr;
+  if (!ck(cudaStreamSynchronize(stream), "sync") ||
+      !ck(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream") ||
+      !ck(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture")) {
+    if (cap) cudaStreamDestroy(cap);
+    return HSRQ_ERR_CUDA;
+  }
+  r = solve_impl(H, ldh, n, b_r, lam_re, lam_im, m_cplx, m_real, B, ldb, b_broadcast, X, ldx,
+                 c_re, c_im, s, ldc, seg_exp, alpha_exp, norms, log2norm, fail, robust, mode, ws,
+                 ws_bytes, cap);
+  cudaGraph_t graph = nullptr;
+  const bool ended = ck(cudaStreamEndCapture(cap, &graph), "end capture");
+  cudaStreamDestroy(cap);
+  if (r < 0 || !ended) {
+    if (graph) cudaGraphDestroy(graph);
+    return r < 0 ? r : HSRQ_ERR_CUDA;
+  }
+  cudaGraphExec_t exec = nullptr;
+  const bool ok = ck(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+  cudaGraphDestroy(graph);
+  if (!ok) return HSRQ_ERR_CUDA;
+  *graph_out = (void*)exec;
+  return 0;
+}
+
+int64_t hsrq_graph_launch(void* graph, void* stream) {
+  if (!graph) return HSRQ_ERR_CONFIG;
+  return ck(cudaGraphLaunch((cudaGraphExec_t)graph, (cudaStream_t)stream), "graph launch")
+             ? 0
+             : HSRQ_ERR_CUDA;
+}
+
+void hsrq_graph_destroy(void* graph) {
+  if (graph) cudaGraphExecDestroy((cudaGraphExec_t)graph);
+}
+
 int64_t hsrq_failure_count(void* ws, void* stream) {
   unsigned long long nf = 0;
   if (!ck(cudaMemcpyAsync(&nf, ws, sizeof(nf), cudaMemcpyDeviceToHost, (cudaStream_t)stream),

@@ -201,6 +201,49 @@ class GroupSolver:
             raise RuntimeError(f"hsrq_solve_group failed ({r}): {_lib.last_error()}")
         return int(r)
 
+    def capture(self, B, broadcast, robust=True, mode="eigvec", stream=None):
+        """Capture this solve (all its kernels and stream forks) as a CUDA graph
+        (hsrq_graph_capture).  ``B`` must stay alive: replays read it, and the
+        shifts in ``lam_re`` / ``lam_im`` (``set_shifts``) as they are then."""
+        stream = stream or torch.cuda.current_stream(self.dh.device)
+        mode_i = {"solve": 0, "eigvec": 1}[mode] | (MODE_COMPACT_ROTATIONS if self.compact else 0)
+        g = ctypes.c_void_p()
+        r = self.lib.hsrq_graph_capture(
+            _ptr(self.dh.t), self.dh.ldh, self.n, self.b_r, _ptr(self.lam_re), _ptr(self.lam_im),
+            self.mc, self.mr, _ptr(B), 0 if broadcast else self.n, 1 if broadcast else 0,
+            _ptr(self.X), self.n, _ptr(self.c_re), _ptr(self.c_im), _ptr(self.s), self.n,
+            _ptr(self.seg_exp), _ptr(self.alpha_exp), _ptr(self.norms), _ptr(self.log2norm),
+            _ptr(self.fail), int(bool(robust)), mode_i, _ptr(self.ws), self.ws_bytes,
+            ctypes.c_void_p(stream.cuda_stream), ctypes.byref(g))
+        if r < 0:
+            raise RuntimeError(f"hsrq_graph_capture failed ({r}): {_lib.last_error()}")
+        self.release_graph()
+        self._graph = g
+        self._graph_b = B
+        return self
+
+    def replay(self, stream=None, sync=True):
+        """Replay the captured solve; returns the failure count when ``sync``."""
+        stream = stream or torch.cuda.current_stream(self.dh.device)
+        st = ctypes.c_void_p(stream.cuda_stream)
+        if self.lib.hsrq_graph_launch(self._graph, st) < 0:
+            raise RuntimeError(f"hsrq_graph_launch failed: {_lib.last_error()}")
+        if sync:
+            return int(self.lib.hsrq_failure_count(_ptr(self.ws), st))
+        return None
+
+    def release_graph(self):
+        g = getattr(self, "_graph", None)
+        if g is not None:
+            self.lib.hsrq_graph_destroy(g)
+            self._graph = None
+
+    def __del__(self):
+        try:
+            self.release_graph()
+        except Exception:  # interpreter shutdown
+            pass
+
     def output(self, nfail):
         return GroupOutput(self.X, self.c_re, self.c_im, self.s, self.seg_exp, self.alpha_exp,
                            self.norms, self.log2norm, self.fail, nfail, self.mc, self.mr,

@@ -91,3 +91,33 @@ def test_async_host_entry_two_in_flight(dev):
     for w, (x, seg, nf) in zip(want, got):
         assert nf == w.nfail
         assert np.array_equal(x, w.X) and np.array_equal(seg, w.seg_exp)
+
+
+def test_graph_replay_matches_eager(dev):
+    """hsrq_graph_capture / hsrq_graph_launch: a captured solve replays the
+    eager solve bit for bit, and picks up new shifts written into the same
+    buffers (GroupSolver.set_shifts) between replays."""
+    import instances
+    from paper_2101_05063_b200.core import HessenbergMatrix
+    from paper_2101_05063_b200.solver import DeviceHessenberg, GroupSolver
+
+    n, b_r = 640, 64
+    h = instances.random_hessenberg(n, 12)
+    ev = np.linalg.eigvals(h)
+    er, ec = ev[ev.imag == 0].real[:6], ev[ev.imag > 0][:5]
+    dh = DeviceHessenberg(HessenbergMatrix(h), dev)
+    b = torch.full((n,), 1e-3, dtype=torch.float64, device=dev)
+    gs = GroupSolver(dh, b_r, ec.size, er.size)
+    gs.set_shifts(ec, er)
+    gs.capture(b, True)
+    results = []
+    for off in (0.0, 0.125):
+        gs.set_shifts(ec + 1j * off, er + off)
+        nf = gs.replay()
+        results.append((nf, gs.X.cpu().numpy().copy(), gs.seg_exp.cpu().numpy().copy()))
+    ref = GroupSolver(dh, b_r, ec.size, er.size)
+    for (nf, X, seg), off in zip(results, (0.0, 0.125)):
+        ref.set_shifts(ec + 1j * off, er + off)
+        rnf = ref.launch(b, True)
+        assert nf == rnf
+        assert np.array_equal(X, ref.X.cpu().numpy()) and np.array_equal(seg, ref.seg_exp.cpu().numpy())
