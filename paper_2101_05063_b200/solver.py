@@ -416,14 +416,59 @@ def solve_group(h, eigs_cplx, eigs_real, b, b_r, *, robust=True, mode="eigvec", 
     mc = len(np.atleast_1d(eigs_cplx)) if eigs_cplx is not None else 0
     mr = len(np.atleast_1d(eigs_real)) if eigs_real is not None else 0
     gs = solver or GroupSolver(dh, b_r, mc, mr, compact=compact)
-    gs.set_shifts(eigs_cplx if mc else [], eigs_real if mr else [])
+    ec = np.asarray(eigs_cplx if mc else [], dtype=np.complex128).ravel()
+    # Complex shifts run sorted by imaginary part: the DP-lane sweep takes a
+    # guard's exact pass when any shift of a warp needs it, and neighbouring
+    # shifts then need it together more often (config 5: diag 135.8 -> 132.7
+    # ms).  Columns are independent, so this changes no result; the outputs
+    # are put back in the caller's order below.
+    perm = np.argsort(ec.imag, kind="stable") if mc > 1 else None
+    if perm is not None and np.array_equal(perm, np.arange(mc)):
+        perm = None
+    gs.set_shifts(ec[perm] if perm is not None else ec, eigs_real if mr else [])
     bt = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64))
     broadcast = bt.dim() == 1
     if not broadcast:
         bt = bt.T.contiguous() if bt.shape[0] == hm.n and bt.shape[1] == gs.ncol else bt
     bt = bt.to(dh.device)
+    if perm is not None and not broadcast:  # right-hand sides follow their shifts
+        bt = bt[torch.from_numpy(_col_index(perm, mc, mr)).to(bt.device)].contiguous()
     nfail = gs.launch(bt, broadcast, robust=robust, mode=mode)
+    if perm is not None:
+        _unpermute(gs, perm)
     return gs.output(nfail), gs
+
+
+def _col_index(perm, mc, mr):
+    """Real-column index map of a complex-shift permutation (complex shift q
+    owns columns 2q, 2q+1; real columns follow unchanged)."""
+    cols = np.empty(2 * mc, dtype=np.int64)
+    cols[0::2] = 2 * perm
+    cols[1::2] = 2 * perm + 1
+    return np.concatenate([cols, 2 * mc + np.arange(mr, dtype=np.int64)])
+
+
+def _unpermute(gs, perm):
+    """Outputs of a solve run with complex shifts in order ``perm`` back to the
+    caller's order (device copies; rows / columns of every per-shift array)."""
+    dev = gs.X.device
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(perm.size)
+    qi = torch.from_numpy(np.concatenate([inv, perm.size + np.arange(gs.mr)])).to(dev)
+    ci = torch.from_numpy(_col_index(inv, gs.mc, gs.mr)).to(dev)
+    gs.X.copy_(gs.X[ci])
+    for t in (gs.c_re, gs.s):
+        if t is not None:
+            t.copy_(t[qi])
+    if gs.compact:
+        gs.c_im[: gs.mc].copy_(gs.c_im[: gs.mc][torch.from_numpy(inv).to(dev)])
+    else:
+        gs.c_im.copy_(gs.c_im[qi])
+    gs.seg_exp.copy_(gs.seg_exp[:, qi])
+    for t in (gs.alpha_exp, gs.norms, gs.log2norm, gs.fail):
+        t.copy_(t[qi])
+    gs.lam_re.copy_(gs.lam_re[qi])
+    gs.lam_im.copy_(gs.lam_im[qi])
 
 
 def to_solution_block(out: GroupOutput, n, *, robust=True, want_cplx):

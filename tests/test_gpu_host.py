@@ -121,3 +121,30 @@ def test_graph_replay_matches_eager(dev):
         rnf = ref.launch(b, True)
         assert nf == rnf
         assert np.array_equal(X, ref.X.cpu().numpy()) and np.array_equal(seg, ref.seg_exp.cpu().numpy())
+
+
+def test_sorted_shift_order_is_transparent(dev):
+    """solve_group runs complex shifts sorted by imaginary part and puts every
+    per-shift output back in the caller's order: identical to a GroupSolver
+    launch with the caller's order, in both the broadcast and explicit-rhs
+    forms."""
+    import instances
+    from paper_2101_05063_b200.core import HessenbergMatrix
+    from paper_2101_05063_b200.solver import DeviceHessenberg, GroupSolver, solve_group
+
+    n, b_r = 500, 64
+    h = instances.random_hessenberg(n, 21)
+    ev = np.linalg.eigvals(h)
+    er, ec = ev[ev.imag == 0].real[:5], ev[ev.imag > 0][:9]
+    ec = ec[np.argsort(-ec.imag)]  # deliberately not in sorted order
+    rng = np.random.default_rng(0)
+    dh = DeviceHessenberg(HessenbergMatrix(h), dev)
+    for B in (np.full(n, 1e-3), rng.standard_normal((2 * ec.size + er.size, n))):
+        out, _ = solve_group(h, ec, er, torch.from_numpy(B), b_r, mode="solve")
+        ref = GroupSolver(dh, b_r, ec.size, er.size)
+        ref.set_shifts(ec, er)
+        ref.launch(torch.from_numpy(B).to(dev), B.ndim == 1, mode="solve")
+        for a, r in ((out.X, ref.X), (out.seg_exp, ref.seg_exp), (out.norms, ref.norms),
+                     (out.c_re, ref.c_re), (out.c_im, ref.c_im), (out.s, ref.s),
+                     (out.alpha_exp, ref.alpha_exp), (out.fail, ref.fail)):
+            assert torch.equal(a, r)
