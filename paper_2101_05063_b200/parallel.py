@@ -32,13 +32,17 @@ def shard_bounds(n_real, n_cplx, world):
 
 
 def local_selection(eigenvalues, rank, world):
-    """This rank's shifts (original indices, values) of a mixed selection."""
+    """This rank's shifts (original indices, values) of a mixed selection:
+    every world-th shift of each kind, in the order sorted by imaginary part
+    -- the same counts as ``shard_bounds`` gives, but each rank a
+    representative sample (the guard work of the diagonal sweeps varies along
+    the spectrum, and the slowest rank sets the step time)."""
     eigs = np.asarray(eigenvalues, dtype=np.complex128).ravel()
     is_cplx = eigs.imag != 0.0
     ridx = np.nonzero(~is_cplx)[0]
     cidx = np.nonzero(is_cplx)[0]
-    rc, cc = shard_bounds(ridx.size, cidx.size, world)
-    idx = np.concatenate([ridx[rc[rank]:rc[rank + 1]], cidx[cc[rank]:cc[rank + 1]]])
+    cidx = cidx[np.argsort(eigs[cidx].imag, kind="stable")]
+    idx = np.concatenate([ridx[rank::world], cidx[rank::world]])
     return idx, eigs[idx]
 
 
