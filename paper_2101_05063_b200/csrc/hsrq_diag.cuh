@@ -380,6 +380,76 @@ __global__ void __launch_bounds__(DW * 32) k_diag_real(Ctx c, DiagArgs a) {
 #undef XX
 }
 
+// Panel operands of a complex shift after its sweep (cupdate_crupdate
+// :645-666; W complex, P real): W_j, Z, the step scalars (chain-warp /
+// whole-warp code shared by k_diag_cplx and k_diag_cplx_ws).
+template <int DP>
+__device__ __forceinline__ void diag_cplx_operands(const Ctx& c, const DiagArgs& a, int64_t q,
+                                                   int64_t col, bool live, int pl, int grp, int k,
+                                                   double* Xr, double* Xi, double* Vr, double* Vi,
+                                                   double c0r, double c0i, double s0, cplx x0) {
+  constexpr int DG = 32 / DP;
+#define IX(i) ((i) * DG + grp)
+  double* bw_re = c.Bop + (2 * col) * KP;
+  double* bz_re = c.Bop + (2 * col + 1) * KP;
+  double* bw_im = c.Bop + (2 * (col + 1)) * KP;
+  double* bz_im = c.Bop + (2 * (col + 1) + 1) * KP;
+  const int64_t qs = live ? q : 0;
+  const double* crow = c.c_re + qs * c.ldc + a.rot_off;
+  const double* cirow = c.c_im + qs * c.ldc + a.rot_off;
+  const double* srow = c.s + qs * c.ldc + a.rot_off;
+  double pre = 1.0;
+  cplx carry = mk(c0r * x0.re + c0i * x0.im, c0r * x0.im - c0i * x0.re);
+  for (int j = 0; j < k; j++) {
+    const double cr = crow[j], ci = cirow[j], sj = srow[j];
+    if (live && pl == (j % DP)) {
+      bw_re[j] = cr * pre;
+      bw_im[j] = ci * pre;
+    }
+    pre = pre * sj;
+    if (j >= 1) {
+      const cplx t2 = mk(Xr[IX(j)], Xi[IX(j)]), t1 = carry;
+      const cplx zf = mk((cr * t1.re - ci * t1.im) - sj * t2.re, (cr * t1.im + ci * t1.re) - sj * t2.im);
+      carry = mk(sj * t1.re + (cr * t2.re + ci * t2.im), sj * t1.im + (cr * t2.im - ci * t2.re));
+      if (pl == (j % DP)) {
+        if (live) {
+          bz_re[j] = zf.re;
+          bz_im[j] = zf.im;
+        }
+        Vr[IX(j - 1)] = zf.re;
+        Vi[IX(j - 1)] = zf.im;
+      }
+    }
+  }
+  __syncwarp();
+  double zm = 0.0;
+  for (int i = pl; i < k - 1; i += DP) {
+    const double z = cabs_(mk(Vr[IX(i)], Vi[IX(i)]));
+    if (z > zm) zm = z;
+  }
+  zm = gmax<DP>(zm);
+  if (live) {
+    for (int j = k + pl; j < KP; j += DP) {
+      bw_re[j] = bw_im[j] = 0.0;
+      bz_re[j] = bz_im[j] = 0.0;
+    }
+    if (pl == 0) {
+      bz_re[0] = bz_im[0] = 0.0;
+      StepScalars st;
+      st.rho_re = s0 * x0.re;
+      st.rho_im = s0 * x0.im;
+      st.zk_re = carry.re;
+      st.zk_im = carry.im;
+      st.zmax = zm;
+      st.P = pre;
+      st.c0_re = c0r;
+      st.c0_im = c0i;
+      c.SS[q] = st;
+    }
+  }
+#undef IX
+}
+
 // ---------------------------------------------------------------------------
 // complex shifts (Im > 0), interleaved re/im columns 2q, 2q+1
 // ---------------------------------------------------------------------------
@@ -669,63 +739,6 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
   if (live && pl == 0) c.E[(int64_t)a.jt * c.ms + q] += gexp;
   if (a.jt == 0) return;
 
-  // ---- panel operands (cupdate_crupdate :645-666; W complex, P real) ----
-  double* bw_re = c.Bop + (2 * col) * KP;
-  double* bz_re = c.Bop + (2 * col + 1) * KP;
-  double* bw_im = c.Bop + (2 * (col + 1)) * KP;
-  double* bz_im = c.Bop + (2 * (col + 1) + 1) * KP;
-  const int64_t qs = live ? q : 0;
-  const double* crow = c.c_re + qs * c.ldc + a.rot_off;
-  const double* cirow = c.c_im + qs * c.ldc + a.rot_off;
-  const double* srow = c.s + qs * c.ldc + a.rot_off;
-  double pre = 1.0;
-  cplx carry = mk(c0r * x0.re + c0i * x0.im, c0r * x0.im - c0i * x0.re);
-  for (int j = 0; j < k; j++) {
-    const double cr = crow[j], ci = cirow[j], sj = srow[j];
-    if (live && pl == (j % DP)) {
-      bw_re[j] = cr * pre;
-      bw_im[j] = ci * pre;
-    }
-    pre = pre * sj;
-    if (j >= 1) {
-      const cplx t2 = mk(Xr[IX(j)], Xi[IX(j)]), t1 = carry;
-      const cplx zf = mk((cr * t1.re - ci * t1.im) - sj * t2.re, (cr * t1.im + ci * t1.re) - sj * t2.im);
-      carry = mk(sj * t1.re + (cr * t2.re + ci * t2.im), sj * t1.im + (cr * t2.im - ci * t2.re));
-      if (pl == (j % DP)) {
-        if (live) {
-          bz_re[j] = zf.re;
-          bz_im[j] = zf.im;
-        }
-        Vr[IX(j - 1)] = zf.re;
-        Vi[IX(j - 1)] = zf.im;
-      }
-    }
-  }
-  __syncwarp();
-  double zm = 0.0;
-  for (int i = pl; i < k - 1; i += DP) {
-    const double z = cabs_(mk(Vr[IX(i)], Vi[IX(i)]));
-    if (z > zm) zm = z;
-  }
-  zm = gmax<DP>(zm);
-  if (live) {
-    for (int j = k + pl; j < KP; j += DP) {
-      bw_re[j] = bw_im[j] = 0.0;
-      bz_re[j] = bz_im[j] = 0.0;
-    }
-    if (pl == 0) {
-      bz_re[0] = bz_im[0] = 0.0;
-      StepScalars st;
-      st.rho_re = s0 * x0.re;
-      st.rho_im = s0 * x0.im;
-      st.zk_re = carry.re;
-      st.zk_im = carry.im;
-      st.zmax = zm;
-      st.P = pre;
-      st.c0_re = c0r;
-      st.c0_im = c0i;
-      c.SS[q] = st;
-    }
-  }
+  diag_cplx_operands<DP>(c, a, q, col, live, pl, grp, k, Xr, Xi, Vr, Vi, c0r, c0i, s0, x0);
 #undef IX
 }

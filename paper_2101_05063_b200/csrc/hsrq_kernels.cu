@@ -252,6 +252,7 @@ __global__ void k_zero_bop(double* Bop, int64_t count) {
 }
 
 #include "hsrq_diag.cuh"
+#include "hsrq_diag_ws.cuh"
 
 #include "hsrq_panel.cuh"
 
@@ -383,6 +384,13 @@ struct DiagVariant {
   int dp, dw;
 };
 DiagVariant g_force_r = {0, 0}, g_force_c = {0, 0};
+int g_diag_ws = -1;  // complex sweep warp pairs per CTA (k_diag_cplx_ws); 0 = off
+
+template <int DP, int NP>
+size_t diag_ws_smem() {
+  return sizeof(double) * (MAXK + NP * (4 * MAXK * (32 / DP) + 3 * MAXK + 32 * (32 / DP)));
+}
+#define HSRQ_DIAG_WS(X) X(4, 1) X(4, 2) X(4, 3) X(8, 2) X(8, 3) X(8, 4) X(16, 2) X(16, 4) X(32, 4) X(32, 8)
 
 template <int DP, int DW, bool CPLX>
 size_t diag_smem() {
@@ -413,10 +421,18 @@ bool diag_attrs() {
   bool ok = true;
 #define HSRQ_ATTR_R(DP, DW)                                                                       ok = ok && ck(cudaFuncSetAttribute(k_diag_real<DP, DW>,                                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,                                                    (int)diag_smem<DP, DW, false>()), "attr diag r");
 #define HSRQ_ATTR_C(DP, DW)                                                                       ok = ok && ck(cudaFuncSetAttribute(k_diag_cplx<DP, DW>,                                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,                                                    (int)diag_smem<DP, DW, true>()), "attr diag c");
+#define HSRQ_ATTR_W(DP, NP)                                                                \
+  ok = ok && ck(cudaFuncSetAttribute(k_diag_cplx_ws<DP, NP>,                               \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                                     (int)diag_ws_smem<DP, NP>()),                         \
+                "attr diag ws");
   HSRQ_DIAG_REAL(HSRQ_ATTR_R)
   HSRQ_DIAG_CPLX(HSRQ_ATTR_C)
+  HSRQ_DIAG_WS(HSRQ_ATTR_W)
 #undef HSRQ_ATTR_R
 #undef HSRQ_ATTR_C
+#undef HSRQ_ATTR_W
+  if (const char* w = getenv("HSRQ_DIAG_WS")) g_diag_ws = atoi(w);
   done = ok;
   return done;
 }
@@ -457,8 +473,28 @@ void diag_launch_c(const Ctx& c, const DiagArgs& a, cudaStream_t s) {
                         diag_smem<DP, DW, true>(), s>>>(c, a);
 }
 
+template <int DP, int NP>
+void diag_launch_ws(const Ctx& c, const DiagArgs& a, cudaStream_t s) {
+  const int per = NP * (32 / DP);
+  k_diag_cplx_ws<DP, NP><<<(unsigned)((a.count + per - 1) / per), NP * 64, diag_ws_smem<DP, NP>(),
+                           s>>>(c, a);
+}
+
 void diag_launch(bool cplx, const Ctx& c, const DiagArgs& a, cudaStream_t s) {
   const DiagVariant v = diag_pick(cplx, a.count);
+  // warp-specialised complex sweep: automatic at DP 4 (all of config 5 on
+  // one GPU: 506 -> 495 ms); measured no gain at DP >= 8 (the lookahead
+  // shards), where the sweep runs beside the panel
+  const int np = g_diag_ws >= 0 ? g_diag_ws : (g_force_c.dp == 0 && v.dp == 4 ? 2 : 0);
+  if (cplx && np > 0) {
+#define HSRQ_LAUNCH_W(DP, NP)         \
+  if (v.dp == DP && np == NP) {       \
+    diag_launch_ws<DP, NP>(c, a, s);  \
+    return;                           \
+  }
+    HSRQ_DIAG_WS(HSRQ_LAUNCH_W)
+#undef HSRQ_LAUNCH_W
+  }
 #define HSRQ_LAUNCH_R(DP, DW)         \
   if (v.dp == DP && v.dw == DW) {     \
     diag_launch_r<DP, DW>(c, a, s);   \
@@ -1251,6 +1287,15 @@ int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset) {
   return 0;
 }
 void hsrq_set_timing(int32_t enable) { g_timing = enable; }
+
+int32_t hsrq_tune_diag(int32_t dp, int32_t dwr, int32_t dwc, int32_t ws) {
+  diag_attrs();  // reads the environment once; the explicit setting wins
+  g_force_r = DiagVariant{dp, dwr};
+  g_force_c = DiagVariant{dp, dwc};
+  if (dp == 0) g_force_r = g_force_c = DiagVariant{0, 0};
+  g_diag_ws = ws;
+  return 0;
+}
 void hsrq_phase_times(double* out_host) {
   for (int i = 0; i < 5; i++) g_phase_ms[i] = 0.0;
   drain_timing(g_phase_ms);

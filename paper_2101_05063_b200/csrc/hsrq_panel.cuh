@@ -180,6 +180,10 @@ __device__ __forceinline__ bool scalars_step2_is_one(const Ctx& c, int jt, int i
   return protect_update_is_one(xbound, c.RS[(int64_t)jt * c.N + it], zmax, c.omega);
 }
 
+#ifndef SEG_UNROLL
+#define SEG_UNROLL 4
+#endif
+constexpr int kSegUnroll = SEG_UNROLL;
 // Max over a tile-row segment of X' = fb b + rho h0 (- lambda rho on the
 // shifted tile's last row): real -> exact max|X'|; complex -> (bound
 // max(|re|+|im|), max of the squared moduli scaled by sc).  Rows are read
@@ -209,7 +213,7 @@ __device__ __forceinline__ void seg_xprime_max(const double* __restrict__ Xr,
     const double2* X2 = reinterpret_cast<const double2*>(Xr);
     const double2* I2 = reinterpret_cast<const double2*>(Xi);
     const double2* H2 = reinterpret_cast<const double2*>(H0);
-#pragma unroll 4
+#pragma unroll kSegUnroll
     for (int r2 = 0; r2 < nrow / 2; r2++) {
       const double2 x = X2[r2], h = H2[r2];
       const double2 y = CPLX ? I2[r2] : make_double2(0.0, 0.0);

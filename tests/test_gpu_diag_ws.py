@@ -1,0 +1,73 @@
+"""The warp-specialised complex diagonal sweep (k_diag_cplx_ws, a warp pair
+per group of shifts: pivot chain beside the previous step's row update) gives
+bit-identical results to the one-warp sweep (k_diag_cplx), which the other
+parity tests pin to the oracle -- on cases that take the guards' rescaling
+and exact-certification paths, at every supported lanes-per-shift."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda", 0)
+
+
+@pytest.fixture
+def lib(dev):
+    from paper_2101_05063_b200 import _lib
+
+    L = _lib.load()
+    yield L
+    L.hsrq_tune_diag(0, 0, 0, -1)  # back to the automatic choice
+
+
+def _outputs(gs):
+    return [t.cpu().numpy().copy() for t in (gs.X, gs.seg_exp, gs.alpha_exp, gs.norms, gs.c_re,
+                                              gs.c_im, gs.s, gs.fail)]
+
+
+@pytest.mark.parametrize("n,b_r,seed,kind,mode", [
+    (700, 128, 3, "start", "eigvec"),
+    (515, 100, 2, "huge", "eigvec"),
+    (640, 128, 4, "rhs", "solve"),
+    (600, 128, 5, "graded", "eigvec"),
+    (301, 37, 6, "start", "eigvec"),
+])
+@pytest.mark.parametrize("dp,ws", [(4, 1), (4, 2), (4, 3), (8, 2), (8, 4), (16, 2), (32, 4)])
+def test_ws_sweep_matches_one_warp_sweep(dev, lib, n, b_r, seed, kind, mode, dp, ws):
+    import instances
+    from paper_2101_05063_b200.core import HessenbergMatrix
+    from paper_2101_05063_b200.solver import DeviceHessenberg, GroupSolver
+
+    h = (instances.graded_hessenberg if kind == "graded" else instances.random_hessenberg)(n, seed)
+    ev = np.linalg.eigvals(h)
+    er = ev[ev.imag == 0].real[:7]
+    ec = ev[ev.imag > 0][:45]
+    rng = np.random.default_rng(seed)
+    if kind == "rhs":
+        er, ec = er + 0.125, ec + 0.125j
+        B = torch.from_numpy(rng.standard_normal((2 * ec.size + er.size, n))).to(dev)
+    else:
+        rho = np.finfo(float).eps * np.max(np.sum(np.abs(h), axis=1))
+        B = torch.full((n,), 1e300 if kind == "huge" else rho, dtype=torch.float64, device=dev)
+    dh = DeviceHessenberg(HessenbergMatrix(h), dev)
+    res = {}
+    for w in (0, ws):
+        lib.hsrq_tune_diag(dp, 4, 2 if dp == 4 else 4, w)
+        gs = GroupSolver(dh, b_r, ec.size, er.size)
+        gs.set_shifts(ec, er)
+        nf = gs.launch(B, B.dim() == 1, mode=mode)
+        res[w] = (nf, _outputs(gs))
+    assert res[0][0] == res[ws][0]
+    for a, b in zip(res[0][1], res[ws][1]):
+        assert np.array_equal(a, b, equal_nan=True)
