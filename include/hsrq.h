@@ -218,13 +218,13 @@ void hsrq_set_timing(int32_t enable);
 void hsrq_phase_times(double* out_host);
 
 /* Tuning / test hook for the diagonal-sweep variant (process-wide; the
- * HSRQ_DIAG / HSRQ_DIAG_WS environment variables set the same state).
- * dp = lanes per shift (0 = automatic), dwr / dwc = warps per CTA of the
- * real / complex sweep; ws = warp pairs per CTA of the warp-specialised
- * complex sweep (k_diag_cplx_ws), 0 = off, -1 = automatic (on at DP 4).
- * Every variant computes identical results; unknown combinations fall back
- * to the default kernel.  Returns 0. */
-int32_t hsrq_tune_diag(int32_t dp, int32_t dwr, int32_t dwc, int32_t ws);
+ * HSRQ_DIAG / HSRQ_DIAG_WSR / HSRQ_DIAG_WS environment variables set the
+ * same state).  dp = lanes per shift (0 = automatic), dwr / dwc = warps per
+ * CTA of the real / complex sweep; wsr / wsc = warp pairs per CTA of the
+ * warp-specialised real / complex sweep (k_diag_real_ws / k_diag_cplx_ws),
+ * 0 = off, -1 = automatic.  Every variant computes identical results;
+ * unknown combinations fall back to the default kernel.  Returns 0. */
+int32_t hsrq_tune_diag(int32_t dp, int32_t dwr, int32_t dwc, int32_t wsr, int32_t wsc);
 
 /*
  * Tile-level entry points (parity tests against the reference kernels).

@@ -55,7 +55,7 @@ SIGNATURES = {
     "hsrq_host_wait": (_i64, [_i64]),
     "hsrq_last_launch_count": (_i64, []),
     "hsrq_set_timing": (None, [_i32]),
-    "hsrq_tune_diag": (_i32, [_i32, _i32, _i32, _i32]),
+    "hsrq_tune_diag": (_i32, [_i32, _i32, _i32, _i32, _i32]),
     "hsrq_phase_times": (None, [_p]),
     "hsrq_tile_diag": (
         _i64,

@@ -157,6 +157,119 @@ __device__ __forceinline__ void put_rot(const Ctx& c, const DiagArgs& a, int64_t
   }
 }
 
+// The last step of a real shift's sweep -- cross-tile rotation
+// (reduce_diag :94-105) and the last pivot (:178-192) -- the write-back of
+// x and the panel operands (update_rupdate :246-253); shared by k_diag_real
+// and the chain warp of k_diag_real_ws.
+template <int DP>
+__device__ __forceinline__ void diag_real_tail(const Ctx& c, const DiagArgs& a, int64_t q,
+                                               int64_t col, bool live, int pl, int grp, int k,
+                                               double* V, double* Xs, int gexp, bool robust) {
+  constexpr int DG = 32 / DP;
+  const double omega = c.omega;
+#define VV(i) V[(i) * DG + grp]
+#define XX(i) Xs[(i) * DG + grp]
+  const double v0 = VV(0);
+  double x0 = XX(0);
+  double c0 = 1.0, s0 = 0.0, piv = v0;
+  double hleft0 = 0.0;
+  if (a.has_left) {
+    hleft0 = a.tile_mode ? a.t_hleft[0] : c.H[(a.js - 1) * c.ldh + a.js];
+    const double r = ghypot(hleft0, v0);
+    if (live && r == 0.0) {
+      if (pl == 0) record_fail(c, a, q, HSRQ_KIND_DEGENERATE, 0);
+      live = false;
+    }
+    c0 = v0 / r;
+    s0 = -hleft0 / r;
+    piv = v0 * c0 - hleft0 * s0;
+  }
+  if (live && pl == 0) put_rot(c, a, q, 0, c0, 0.0, s0);
+  if (live && piv == 0.0) {
+    if (pl == 0) record_fail(c, a, q, HSRQ_KIND_SINGULAR, 0);
+    live = false;
+  }
+  if (robust && live) {
+    const double avv = fabs(piv), ax = fabs(x0);
+    if (avv < 1.0 && ax > avv * omega) {
+      const int e = pow2floor_e(avv * omega / ax);
+      const double xi = p2(e);
+      for (int i = pl; i < k; i += DP) XX(i) *= xi;
+      x0 *= xi;
+      gexp += e;
+    }
+  }
+  x0 = x0 / piv;
+  if (pl == 0) XX(0) = x0;
+  __syncwarp();
+  // (no early return: dead or padding groups keep executing so that warp
+  // shuffles stay convergent; their writes are masked by `live`)
+  if (live) {
+    for (int i = pl; i < k; i += DP) {
+      if (a.tile_mode)
+        a.t_x[(int64_t)i * a.t_b + q] = XX(i);
+      else
+        c.X[col * c.ldx + a.js + i] = XX(i);
+    }
+  }
+  if (a.tile_mode) {
+    if (live && pl == 0) a.t_beta[q] += gexp;
+    return;
+  }
+  if (live && pl == 0) c.E[(int64_t)a.jt * c.ms + q] += gexp;
+  if (a.jt == 0) return;
+
+  // ---- panel operands: W_j = c_j prod_{t<j} s_t, P; Z (update_rupdate :246-253) ----
+  double* bw = c.Bop + (2 * col) * KP;
+  double* bz = c.Bop + (2 * col + 1) * KP;
+  const double* crow = c.c_re + (live ? q : 0) * c.ldc + a.rot_off;
+  const double* srow = c.s + (live ? q : 0) * c.ldc + a.rot_off;
+  double pre = 1.0;
+  double carry = c0 * x0;  // Z[0] = c[0] * Z[0]
+  for (int j = 0; j < k; j++) {
+    const double cj = crow[j], sj = srow[j];
+    if (live && pl == (j % DP)) bw[j] = cj * pre;
+    pre = pre * sj;
+    if (j >= 1) {
+      const double t2 = XX(j), t1 = carry;
+      const double zf = cj * t1 - sj * t2;  // final Z[j-1]
+      carry = sj * t1 + cj * t2;
+      if (pl == (j % DP)) {
+        if (live) bz[j] = zf;
+        VV(j - 1) = zf;  // keep Z for zmax
+      }
+    }
+  }
+  __syncwarp();
+  double zm = 0.0;
+  for (int i = pl; i < k - 1; i += DP) {
+    const double z = fabs(VV(i));
+    if (z > zm) zm = z;
+  }
+  zm = gmax<DP>(zm);
+  if (live) {
+    for (int j = k + pl; j < KP; j += DP) {
+      bw[j] = 0.0;
+      bz[j] = 0.0;
+    }
+    if (pl == 0) {
+      bz[0] = 0.0;
+      StepScalars st;
+      st.rho_re = s0 * x0;
+      st.rho_im = 0.0;
+      st.zk_re = carry;
+      st.zk_im = 0.0;
+      st.zmax = zm;
+      st.P = pre;
+      st.c0_re = c0;
+      st.c0_im = 0.0;
+      c.SS[q] = st;
+    }
+  }
+#undef VV
+#undef XX
+}
+
 // ---------------------------------------------------------------------------
 // real shifts
 // ---------------------------------------------------------------------------
@@ -278,104 +391,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_real(Ctx c, DiagArgs a) {
     __syncwarp();
     cur ^= 1;
   }
-  // cross-tile rotation (reduce_diag :94-105) and the last pivot (:178-192)
-  const double v0 = VV(0);
-  double x0 = XX(0);
-  double c0 = 1.0, s0 = 0.0, piv = v0;
-  double hleft0 = 0.0;
-  if (a.has_left) {
-    hleft0 = a.tile_mode ? a.t_hleft[0] : c.H[(a.js - 1) * c.ldh + a.js];
-    const double r = ghypot(hleft0, v0);
-    if (live && r == 0.0) {
-      if (pl == 0) record_fail(c, a, q, HSRQ_KIND_DEGENERATE, 0);
-      live = false;
-    }
-    c0 = v0 / r;
-    s0 = -hleft0 / r;
-    piv = v0 * c0 - hleft0 * s0;
-  }
-  if (live && pl == 0) put_rot(c, a, q, 0, c0, 0.0, s0);
-  if (live && piv == 0.0) {
-    if (pl == 0) record_fail(c, a, q, HSRQ_KIND_SINGULAR, 0);
-    live = false;
-  }
-  if (robust && live) {
-    const double avv = fabs(piv), ax = fabs(x0);
-    if (avv < 1.0 && ax > avv * omega) {
-      const int e = pow2floor_e(avv * omega / ax);
-      const double xi = p2(e);
-      for (int i = pl; i < k; i += DP) XX(i) *= xi;
-      x0 *= xi;
-      gexp += e;
-    }
-  }
-  x0 = x0 / piv;
-  if (pl == 0) XX(0) = x0;
-  __syncwarp();
-  // (no early return: dead or padding groups keep executing so that warp
-  // shuffles stay convergent; their writes are masked by `live`)
-  if (live) {
-    for (int i = pl; i < k; i += DP) {
-      if (a.tile_mode)
-        a.t_x[(int64_t)i * a.t_b + q] = XX(i);
-      else
-        c.X[col * c.ldx + a.js + i] = XX(i);
-    }
-  }
-  if (a.tile_mode) {
-    if (live && pl == 0) a.t_beta[q] += gexp;
-    return;
-  }
-  if (live && pl == 0) c.E[(int64_t)a.jt * c.ms + q] += gexp;
-  if (a.jt == 0) return;
-
-  // ---- panel operands: W_j = c_j prod_{t<j} s_t, P; Z (update_rupdate :246-253) ----
-  double* bw = c.Bop + (2 * col) * KP;
-  double* bz = c.Bop + (2 * col + 1) * KP;
-  const double* crow = c.c_re + (live ? q : 0) * c.ldc + a.rot_off;
-  const double* srow = c.s + (live ? q : 0) * c.ldc + a.rot_off;
-  double pre = 1.0;
-  double carry = c0 * x0;  // Z[0] = c[0] * Z[0]
-  for (int j = 0; j < k; j++) {
-    const double cj = crow[j], sj = srow[j];
-    if (live && pl == (j % DP)) bw[j] = cj * pre;
-    pre = pre * sj;
-    if (j >= 1) {
-      const double t2 = XX(j), t1 = carry;
-      const double zf = cj * t1 - sj * t2;  // final Z[j-1]
-      carry = sj * t1 + cj * t2;
-      if (pl == (j % DP)) {
-        if (live) bz[j] = zf;
-        VV(j - 1) = zf;  // keep Z for zmax
-      }
-    }
-  }
-  __syncwarp();
-  double zm = 0.0;
-  for (int i = pl; i < k - 1; i += DP) {
-    const double z = fabs(VV(i));
-    if (z > zm) zm = z;
-  }
-  zm = gmax<DP>(zm);
-  if (live) {
-    for (int j = k + pl; j < KP; j += DP) {
-      bw[j] = 0.0;
-      bz[j] = 0.0;
-    }
-    if (pl == 0) {
-      bz[0] = 0.0;
-      StepScalars st;
-      st.rho_re = s0 * x0;
-      st.rho_im = 0.0;
-      st.zk_re = carry;
-      st.zk_im = 0.0;
-      st.zmax = zm;
-      st.P = pre;
-      st.c0_re = c0;
-      st.c0_im = 0.0;
-      c.SS[q] = st;
-    }
-  }
+  diag_real_tail<DP>(c, a, q, col, live, pl, grp, k, V, Xs, gexp, robust);
 #undef VV
 #undef XX
 }

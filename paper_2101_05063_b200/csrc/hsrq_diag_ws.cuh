@@ -384,3 +384,186 @@ __global__ void __launch_bounds__(NP * 64) k_diag_cplx_ws(Ctx c, DiagArgs a) {
 #undef XB
 #undef E2
 }
+
+// Real shifts, same pairing (reduce_diag :75-106 + solve_rsolve :133-195).
+// Guard 1 depends only on the pivot and x_kp, so the chain warp resolves it
+// before the barrier and passes the final x_kp / phi and the exponent; guard
+// 2 is protect_update on the bulk warp's exact maxima.
+template <int DP, int NP>
+__global__ void __launch_bounds__(NP * 64) k_diag_real_ws(Ctx c, DiagArgs a) {
+  constexpr int DG = 32 / DP;
+  constexpr int PAIR = 2 * MAXK * DG + 3 * MAXK + 16 * DG;
+  extern __shared__ __align__(16) double dsm[];
+  double* hmax = dsm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, role = warp & 1;
+  const int bar = 1 + pair;
+  const int grp = lane / DP, pl = lane % DP;
+  double* V = dsm + MAXK + pair * PAIR;
+  double* Xs = V + MAXK * DG;
+  double* hb = Xs + MAXK * DG;  // [3][MAXK]
+  double* ex = hb + 3 * MAXK;   // [16][DG]
+#define VV(i) V[(i) * DG + grp]
+#define XX(i) Xs[(i) * DG + grp]
+#define CH(p, s) ex[((p) * 5 + (s)) * DG + grp]
+#define XB(p, s) ex[(10 + (p) * 2 + (s)) * DG + grp]
+  const int k = a.k;
+  load_hmax(c, a, hmax);
+  const int64_t q = a.q0 + ((int64_t)blockIdx.x * NP + pair) * DG + grp;
+  bool live = q < a.q0 + a.count;
+  if (live && !a.tile_mode && c.fail[q] != 0) live = false;
+  const int64_t col = a.tile_mode ? 0 : 2 * c.mc + (q - c.mc);
+  const double lam = live ? c.lam_re[q] : 0.0;
+  const double omega = c.omega;
+  const bool robust = c.robust;
+  auto HB = [&](int t) { return hb + (t % 3) * MAXK; };
+
+  if (role == 1) {
+    double xm = 0.0, vm = 0.0;
+    for (int i = pl; i < k; i += DP) {
+      double vv = 0.0, xx = 0.0;
+      if (live) {
+        if (a.tile_mode) {
+          vv = a.t_rright[(int64_t)i * a.t_b + q];
+          xx = a.t_x[(int64_t)i * a.t_b + q];
+        } else {
+          vv = c.Cr[col * c.ldx + a.js + i];
+          xx = c.X[col * c.ldx + a.js + i];
+        }
+      }
+      VV(i) = vv;
+      XX(i) = xx;
+      if (i < k - 1) {
+        if (fabs(xx) > xm) xm = fabs(xx);
+        if (fabs(vv) > vm) vm = fabs(vv);
+      }
+    }
+    xm = gmax<DP>(xm);
+    vm = gmax<DP>(vm);
+    if (pl == 0 && k >= 2) {
+      XB((k - 1) & 1, 0) = xm;
+      XB((k - 1) & 1, 1) = vm;
+    }
+  } else if (k >= 2) {
+    fill_col(c, a, HB(k - 2), k - 2, k, lane);
+  }
+  pair_sync(bar);
+
+  int gexp = 0;
+  double bcc = 0.0, bss = 0.0, bxk = 0.0;  // bulk warp: step kp+1's rotation and x
+  for (int kp = k - 1; kp >= 1; --kp) {
+    const int p = kp & 1;
+    if (role == 0) {
+      if (kp >= 2) {
+        fill_col(c, a, HB(kp - 2), kp - 2, kp, lane);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      __syncwarp();
+      const double* hcol = HB(kp - 1);
+      const double vk = VV(kp);
+      double xk = XX(kp);
+      const double av = hcol[kp];
+      const double r = ghypot(av, vk);
+      if (live && r == 0.0) {
+        if (pl == 0) record_fail(c, a, q, HSRQ_KIND_DEGENERATE, kp);
+        live = false;
+      }
+      const double cc = vk / r, ss = -av / r;
+      if (live && pl == 0) put_rot(c, a, q, kp, cc, 0.0, ss);
+      const double phi = vk * cc - av * ss;
+      if (live && phi == 0.0) {
+        if (pl == 0) record_fail(c, a, q, HSRQ_KIND_SINGULAR, kp);
+        live = false;
+      }
+      int e1 = 0;
+      if (robust && live) {  // guard 1 (:144-151)
+        const double aphi = fabs(phi), ax = fabs(xk);
+        if (aphi < 1.0 && ax > aphi * omega) {
+          e1 = pow2floor_e(aphi * omega / ax);
+          xk *= p2(e1);
+        }
+      }
+      xk = xk / phi;
+      if (pl == 0) {
+        CH(p, 0) = cc;
+        CH(p, 1) = ss;
+        CH(p, 2) = xk;
+        CH(p, 3) = (double)e1;
+        CH(p, 4) = live ? 1.0 : 0.0;
+      }
+    } else if (kp < k - 1) {
+      // row update of step kp+1 (column kp, rows < kp)
+      const double* hcol = HB(kp);
+      const double tau1 = bss * bxk, tau2 = bcc * bxk;
+      double nxm = 0.0, nvm = 0.0;
+#pragma unroll 1
+      for (int i = pl; i < kp; i += DP) {
+        const double hi = hcol[i];
+        double vv = VV(i), xx = XX(i);
+        xx = (xx - tau2 * vv) + tau1 * hi;
+        vv = bcc * hi + bss * vv;
+        if (fabs(xx) > nxm) nxm = fabs(xx);
+        if (fabs(vv) > nvm) nvm = fabs(vv);
+        VV(i) = vv;
+        XX(i) = xx;
+      }
+      nxm = gmax<DP>(nxm);
+      nvm = gmax<DP>(nvm);
+      if (pl == 0) {
+        XB(p, 0) = nxm;
+        XB(p, 1) = nvm;
+      }
+    }
+    pair_sync(bar);  // P
+
+    const double cc = CH(p, 0), ss = CH(p, 1);
+    double xk = CH(p, 2);
+    const int e1 = (int)CH(p, 3);
+    const bool lv = CH(p, 4) != 0.0;
+    double xm = XB(p, 0);
+    const double vm = XB(p, 1);
+    if (__any_sync(FULL, e1 != 0)) {  // guard 1's rescaling of the other rows
+      if (e1 != 0) {
+        const double xi = p2(e1);
+        for (int i = pl + DP * role; i < k; i += 2 * DP) XX(i) *= xi;
+        xm *= xi;
+        gexp += e1;
+      }
+      pair_sync(bar);
+    }
+    int e2 = 0;
+    if (robust && lv) e2 = protect_update_e(xm, vm + hmax[kp] + fabs(lam), fabs(xk), omega);
+    if (__any_sync(FULL, e2 < 0)) {  // guard 2 (:153-168)
+      if (e2 < 0) {
+        const double xi = p2(e2);
+        for (int i = pl + DP * role; i < k; i += 2 * DP) XX(i) *= xi;
+        xk *= xi;
+        gexp += e2;
+      }
+      pair_sync(bar);
+    }
+    if (role == 0) {
+      if (pl == (kp % DP)) XX(kp) = xk;
+      if (pl == (kp - 1) % DP) {  // the shifted row (diagonal entry h - lambda)
+        const int i = kp - 1;
+        const double hd = HB(kp - 1)[i] - lam;
+        const double vv = VV(i), xx = XX(i);
+        XX(i) = (xx - (cc * xk) * vv) + (ss * xk) * hd;
+        VV(i) = cc * hd + ss * vv;
+      }
+      __syncwarp();
+    } else {
+      bcc = cc;
+      bss = ss;
+      bxk = xk;
+    }
+  }
+  if (role == 1) return;
+  diag_real_tail<DP>(c, a, q, col, live, pl, grp, k, V, Xs, gexp, robust);
+#undef VV
+#undef XX
+#undef CH
+#undef XB
+}

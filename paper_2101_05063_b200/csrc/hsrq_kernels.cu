@@ -384,13 +384,19 @@ struct DiagVariant {
   int dp, dw;
 };
 DiagVariant g_force_r = {0, 0}, g_force_c = {0, 0};
-int g_diag_ws = -1;  // complex sweep warp pairs per CTA (k_diag_cplx_ws); 0 = off
+int g_diag_ws = -1;    // complex sweep warp pairs per CTA (k_diag_cplx_ws); 0 = off
+int g_diag_ws_r = -1;  // real sweep warp pairs per CTA (k_diag_real_ws); 0 = off
 
 template <int DP, int NP>
 size_t diag_ws_smem() {
   return sizeof(double) * (MAXK + NP * (4 * MAXK * (32 / DP) + 3 * MAXK + 32 * (32 / DP)));
 }
+template <int DP, int NP>
+size_t diag_ws_smem_r() {
+  return sizeof(double) * (MAXK + NP * (2 * MAXK * (32 / DP) + 3 * MAXK + 16 * (32 / DP)));
+}
 #define HSRQ_DIAG_WS(X) X(4, 1) X(4, 2) X(4, 3) X(8, 2) X(8, 3) X(8, 4) X(16, 2) X(16, 4) X(32, 4) X(32, 8)
+#define HSRQ_DIAG_WSR(X) X(4, 2) X(4, 3) X(4, 4) X(8, 2) X(8, 4) X(16, 2) X(16, 4) X(32, 4) X(32, 8)
 
 template <int DP, int DW, bool CPLX>
 size_t diag_smem() {
@@ -429,10 +435,18 @@ bool diag_attrs() {
   HSRQ_DIAG_REAL(HSRQ_ATTR_R)
   HSRQ_DIAG_CPLX(HSRQ_ATTR_C)
   HSRQ_DIAG_WS(HSRQ_ATTR_W)
+#define HSRQ_ATTR_WR(DP, NP)                                                               \
+  ok = ok && ck(cudaFuncSetAttribute(k_diag_real_ws<DP, NP>,                               \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                                     (int)diag_ws_smem_r<DP, NP>()),                       \
+                "attr diag wsr");
+  HSRQ_DIAG_WSR(HSRQ_ATTR_WR)
+#undef HSRQ_ATTR_WR
 #undef HSRQ_ATTR_R
 #undef HSRQ_ATTR_C
 #undef HSRQ_ATTR_W
   if (const char* w = getenv("HSRQ_DIAG_WS")) g_diag_ws = atoi(w);
+  if (const char* w = getenv("HSRQ_DIAG_WSR")) g_diag_ws_r = atoi(w);
   done = ok;
   return done;
 }
@@ -474,6 +488,12 @@ void diag_launch_c(const Ctx& c, const DiagArgs& a, cudaStream_t s) {
 }
 
 template <int DP, int NP>
+void diag_launch_ws_r(const Ctx& c, const DiagArgs& a, cudaStream_t s) {
+  const int per = NP * (32 / DP);
+  k_diag_real_ws<DP, NP><<<(unsigned)((a.count + per - 1) / per), NP * 64,
+                           diag_ws_smem_r<DP, NP>(), s>>>(c, a);
+}
+template <int DP, int NP>
 void diag_launch_ws(const Ctx& c, const DiagArgs& a, cudaStream_t s) {
   const int per = NP * (32 / DP);
   k_diag_cplx_ws<DP, NP><<<(unsigned)((a.count + per - 1) / per), NP * 64, diag_ws_smem<DP, NP>(),
@@ -494,6 +514,19 @@ void diag_launch(bool cplx, const Ctx& c, const DiagArgs& a, cudaStream_t s) {
   }
     HSRQ_DIAG_WS(HSRQ_LAUNCH_W)
 #undef HSRQ_LAUNCH_W
+  }
+  // real: only for groups without complex shifts (real-only config 5: 128 ->
+  // 122 ms; beside the complex sweep the extra warps cost more than they save)
+  const int npr = g_diag_ws_r >= 0 ? g_diag_ws_r
+                                   : (c.mc == 0 && g_force_r.dp == 0 && v.dp <= 16 ? 2 : 0);
+  if (!cplx && npr > 0) {
+#define HSRQ_LAUNCH_WR(DP, NP)          \
+  if (v.dp == DP && npr == NP) {        \
+    diag_launch_ws_r<DP, NP>(c, a, s);  \
+    return;                             \
+  }
+    HSRQ_DIAG_WSR(HSRQ_LAUNCH_WR)
+#undef HSRQ_LAUNCH_WR
   }
 #define HSRQ_LAUNCH_R(DP, DW)         \
   if (v.dp == DP && v.dw == DW) {     \
@@ -1288,12 +1321,13 @@ int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset) {
 }
 void hsrq_set_timing(int32_t enable) { g_timing = enable; }
 
-int32_t hsrq_tune_diag(int32_t dp, int32_t dwr, int32_t dwc, int32_t ws) {
+int32_t hsrq_tune_diag(int32_t dp, int32_t dwr, int32_t dwc, int32_t wsr, int32_t wsc) {
   diag_attrs();  // reads the environment once; the explicit setting wins
   g_force_r = DiagVariant{dp, dwr};
   g_force_c = DiagVariant{dp, dwc};
   if (dp == 0) g_force_r = g_force_c = DiagVariant{0, 0};
-  g_diag_ws = ws;
+  g_diag_ws_r = wsr;
+  g_diag_ws = wsc;
   return 0;
 }
 void hsrq_phase_times(double* out_host) {

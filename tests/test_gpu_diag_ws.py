@@ -1,6 +1,6 @@
-"""The warp-specialised complex diagonal sweep (k_diag_cplx_ws, a warp pair
-per group of shifts: pivot chain beside the previous step's row update) gives
-bit-identical results to the one-warp sweep (k_diag_cplx), which the other
+"""The warp-specialised diagonal sweeps (k_diag_real_ws / k_diag_cplx_ws, a warp pair
+per group of shifts: pivot chain beside the previous step's row update) give
+bit-identical results to the one-warp sweeps (k_diag_real / k_diag_cplx), which the other
 parity tests pin to the oracle -- on cases that take the guards' rescaling
 and exact-certification paths, at every supported lanes-per-shift."""
 
@@ -28,7 +28,7 @@ def lib(dev):
 
     L = _lib.load()
     yield L
-    L.hsrq_tune_diag(0, 0, 0, -1)  # back to the automatic choice
+    L.hsrq_tune_diag(0, 0, 0, -1, -1)  # back to the automatic choice
 
 
 def _outputs(gs):
@@ -42,8 +42,9 @@ def _outputs(gs):
     (640, 128, 4, "rhs", "solve"),
     (600, 128, 5, "graded", "eigvec"),
     (301, 37, 6, "start", "eigvec"),
+    (900, 128, 7, "realonly", "eigvec"),
 ])
-@pytest.mark.parametrize("dp,ws", [(4, 1), (4, 2), (4, 3), (8, 2), (8, 4), (16, 2), (32, 4)])
+@pytest.mark.parametrize("dp,ws", [(4, 2), (4, 3), (8, 2), (8, 4), (16, 2), (32, 4)])
 def test_ws_sweep_matches_one_warp_sweep(dev, lib, n, b_r, seed, kind, mode, dp, ws):
     import instances
     from paper_2101_05063_b200.core import HessenbergMatrix
@@ -53,6 +54,9 @@ def test_ws_sweep_matches_one_warp_sweep(dev, lib, n, b_r, seed, kind, mode, dp,
     ev = np.linalg.eigvals(h)
     er = ev[ev.imag == 0].real[:7]
     ec = ev[ev.imag > 0][:45]
+    if kind == "realonly":  # a group without complex shifts
+        er = np.concatenate([ev[ev.imag == 0].real, ev[ev.imag > 0].real[:30] + 1e-3])
+        ec = ec[:0]
     rng = np.random.default_rng(seed)
     if kind == "rhs":
         er, ec = er + 0.125, ec + 0.125j
@@ -63,7 +67,7 @@ def test_ws_sweep_matches_one_warp_sweep(dev, lib, n, b_r, seed, kind, mode, dp,
     dh = DeviceHessenberg(HessenbergMatrix(h), dev)
     res = {}
     for w in (0, ws):
-        lib.hsrq_tune_diag(dp, 4, 2 if dp == 4 else 4, w)
+        lib.hsrq_tune_diag(dp, 4, 2 if dp == 4 else 4, w, w)
         gs = GroupSolver(dh, b_r, ec.size, er.size)
         gs.set_shifts(ec, er)
         nf = gs.launch(B, B.dim() == 1, mode=mode)

@@ -1,7 +1,8 @@
 """Per-rank time of the config-5 sweep for a world size W, measured on ONE GPU
 by running rank 0's shard alone (ranks are independent: no collective inside
 the sweep, parallel.py) -- a proxy for the strong-scaling behaviour.
-python tools/shard_time.py W [W ...]   (HSRQ_DIAG=DP,DWR,DWC selects a variant)"""
+python tools/shard_time.py W [W ...]   (HSRQ_DIAG=DP,DWR,DWC selects a variant;
+SHARD_ONLY=real|cplx keeps one kind of shift)"""
 import ctypes
 import os
 import sys
@@ -24,6 +25,11 @@ L = _lib.load()
 start = torch.full((hm.n,), np.finfo(float).eps * hm.infinity_norm(), dtype=torch.float64, device=dev)
 for W in (int(w) for w in sys.argv[1:]):
     my_r, my_c = bench.partition(er, ec, 0, W)
+    only = os.environ.get("SHARD_ONLY")  # "real" / "cplx": drop the other kind (diagnostics)
+    if only == "real":
+        my_c = my_c[:0]
+    elif only == "cplx":
+        my_r = my_r[:0]
     gs = GroupSolver(dh, b_r, my_c.size, my_r.size)
     gs.set_shifts(my_c, my_r)
     gs.launch(start, True)
