@@ -418,8 +418,12 @@ bool diag_attrs() {
   }
   const char* e = getenv("HSRQ_DIAG");
   if (e) {
-    int dp, dwr, dwc;
-    if (sscanf(e, "%d,%d,%d", &dp, &dwr, &dwc) == 3) {
+    int dp, dwr, dwc, d4;
+    const int got = sscanf(e, "%d,%d,%d,%d", &dp, &dwr, &dwc, &d4);
+    if (got == 4) {  // "DPR,DWR,DPC,DWC": separate lanes per shift
+      g_force_r = DiagVariant{dp, dwr};
+      g_force_c = DiagVariant{dwc, d4};
+    } else if (got == 3) {
       g_force_r = DiagVariant{dp, dwr};
       g_force_c = DiagVariant{dp, dwc};
     }
