@@ -226,19 +226,41 @@ __device__ __forceinline__ void diag_real_tail(const Ctx& c, const DiagArgs& a, 
   const double* srow = c.s + (live ? q : 0) * c.ldc + a.rot_off;
   double pre = 1.0;
   double carry = c0 * x0;  // Z[0] = c[0] * Z[0]
-  for (int j = 0; j < k; j++) {
-    const double cj = crow[j], sj = srow[j];
-    if (live && pl == (j % DP)) bw[j] = cj * pre;
-    pre = pre * sj;
-    if (j >= 1) {
-      const double t2 = XX(j), t1 = carry;
-      const double zf = cj * t1 - sj * t2;  // final Z[j-1]
-      carry = sj * t1 + cj * t2;
-      if (pl == (j % DP)) {
-        if (live) bz[j] = zf;
-        VV(j - 1) = zf;  // keep Z for zmax
+  // rotations j = jb + pl loaded by lane pl one chunk of DP ahead and
+  // broadcast within the group: the serial carry chain no longer waits on
+  // an L2 round trip per j
+  const int gb = grp * DP;
+  double lc = 1.0, ls = 0.0;
+  if (pl < k) {
+    lc = crow[pl];
+    ls = srow[pl];
+  }
+  for (int jb = 0; jb < k; jb += DP) {
+    double nc = 1.0, ns = 0.0;
+    if (jb + DP + pl < k) {
+      nc = crow[jb + DP + pl];
+      ns = srow[jb + DP + pl];
+    }
+#pragma unroll(DP > 8 ? 8 : DP)
+    for (int t = 0; t < DP; t++) {
+      const int j = jb + t;
+      const double cj = __shfl_sync(FULL, lc, gb + t), sj = __shfl_sync(FULL, ls, gb + t);
+      if (j < k) {
+        if (live && pl == t) bw[j] = cj * pre;
+        pre = pre * sj;
+        if (j >= 1) {
+          const double t2 = XX(j), t1 = carry;
+          const double zf = cj * t1 - sj * t2;  // final Z[j-1]
+          carry = sj * t1 + cj * t2;
+          if (pl == t) {
+            if (live) bz[j] = zf;
+            VV(j - 1) = zf;  // keep Z for zmax
+          }
+        }
       }
     }
+    lc = nc;
+    ls = ns;
   }
   __syncwarp();
   double zm = 0.0;
@@ -416,26 +438,52 @@ __device__ __forceinline__ void diag_cplx_operands(const Ctx& c, const DiagArgs&
   const double* srow = c.s + qs * c.ldc + a.rot_off;
   double pre = 1.0;
   cplx carry = mk(c0r * x0.re + c0i * x0.im, c0r * x0.im - c0i * x0.re);
-  for (int j = 0; j < k; j++) {
-    const double cr = crow[j], ci = cirow[j], sj = srow[j];
-    if (live && pl == (j % DP)) {
-      bw_re[j] = cr * pre;
-      bw_im[j] = ci * pre;
+  // rotations prefetched one chunk ahead by lane pl (j = jb + pl) and
+  // broadcast within the group (see diag_real_tail)
+  const int gb = grp * DP;
+  double lc = 1.0, lci = 0.0, ls = 0.0;
+  if (pl < k) {
+    lc = crow[pl];
+    lci = cirow[pl];
+    ls = srow[pl];
+  }
+  for (int jb = 0; jb < k; jb += DP) {
+    double nc = 1.0, nci = 0.0, ns = 0.0;
+    if (jb + DP + pl < k) {
+      nc = crow[jb + DP + pl];
+      nci = cirow[jb + DP + pl];
+      ns = srow[jb + DP + pl];
     }
-    pre = pre * sj;
-    if (j >= 1) {
-      const cplx t2 = mk(Xr[IX(j)], Xi[IX(j)]), t1 = carry;
-      const cplx zf = mk((cr * t1.re - ci * t1.im) - sj * t2.re, (cr * t1.im + ci * t1.re) - sj * t2.im);
-      carry = mk(sj * t1.re + (cr * t2.re + ci * t2.im), sj * t1.im + (cr * t2.im - ci * t2.re));
-      if (pl == (j % DP)) {
-        if (live) {
-          bz_re[j] = zf.re;
-          bz_im[j] = zf.im;
+#pragma unroll(DP > 8 ? 8 : DP)
+    for (int t = 0; t < DP; t++) {
+      const int j = jb + t;
+      const double cr = __shfl_sync(FULL, lc, gb + t), ci = __shfl_sync(FULL, lci, gb + t);
+      const double sj = __shfl_sync(FULL, ls, gb + t);
+      if (j < k) {
+        if (live && pl == t) {
+          bw_re[j] = cr * pre;
+          bw_im[j] = ci * pre;
         }
-        Vr[IX(j - 1)] = zf.re;
-        Vi[IX(j - 1)] = zf.im;
+        pre = pre * sj;
+        if (j >= 1) {
+          const cplx t2 = mk(Xr[IX(j)], Xi[IX(j)]), t1 = carry;
+          const cplx zf = mk((cr * t1.re - ci * t1.im) - sj * t2.re,
+                             (cr * t1.im + ci * t1.re) - sj * t2.im);
+          carry = mk(sj * t1.re + (cr * t2.re + ci * t2.im), sj * t1.im + (cr * t2.im - ci * t2.re));
+          if (pl == t) {
+            if (live) {
+              bz_re[j] = zf.re;
+              bz_im[j] = zf.im;
+            }
+            Vr[IX(j - 1)] = zf.re;
+            Vi[IX(j - 1)] = zf.im;
+          }
+        }
       }
     }
+    lc = nc;
+    lci = nci;
+    ls = ns;
   }
   __syncwarp();
   double zm = 0.0;
