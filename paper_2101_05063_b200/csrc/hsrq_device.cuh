@@ -135,6 +135,54 @@ __device__ __forceinline__ int protect_update_e(double bnorm, double hnorm, doub
   return e;
 }
 
+// protect_update_e at two argument pairs with the same xnorm (the guard-2
+// interval ends), evaluated side by side so the two division chains and
+// halving loops overlap; each result equals protect_update_e's.
+__device__ __forceinline__ void protect_update_e2(double bn1, double hn1, double bn2, double hn2,
+                                                  double xnorm, double omega, int& r1, int& r2) {
+  bool z1, z2;
+  double c1, c2;
+  if (xnorm <= 1.0) {
+    z1 = bn1 + hn1 * xnorm <= omega;
+    z2 = bn2 + hn2 * xnorm <= omega;
+    c1 = (omega * 0.5) / (bn1 * 0.5 + (hn1 * xnorm) * 0.5);
+    c2 = (omega * 0.5) / (bn2 * 0.5 + (hn2 * xnorm) * 0.5);
+  } else {
+    z1 = bn1 <= omega && hn1 <= (omega - bn1) / xnorm;
+    z2 = bn2 <= omega && hn2 <= (omega - bn2) / xnorm;
+    const double u1 = bn1 / xnorm, u2 = bn2 / xnorm;
+    c1 = ((omega * 0.5) / (u1 * 0.5 + hn1 * 0.5)) / xnorm;
+    c2 = ((omega * 0.5) / (u2 * 0.5 + hn2 * 0.5)) / xnorm;
+  }
+  if (!(c1 > 0.0)) c1 = 0x1p-1074;
+  if (c1 > 1.0) c1 = 1.0;
+  if (!(c2 > 0.0)) c2 = 0x1p-1074;
+  if (c2 > 1.0) c2 = 1.0;
+  int e1 = pow2floor_e(c1), e2 = pow2floor_e(c2);
+  double x1 = p2(e1), x2 = p2(e2);
+  bool d1 = z1, d2 = z2;
+  for (int it = 0; it < 200 && !(d1 && d2); it++) {
+    if (!d1) {
+      if (x1 * bn1 + hn1 * (x1 * xnorm) <= omega) {
+        d1 = true;
+      } else {
+        x1 *= 0.5;
+        e1 -= 1;
+      }
+    }
+    if (!d2) {
+      if (x2 * bn2 + hn2 * (x2 * xnorm) <= omega) {
+        d2 = true;
+      } else {
+        x2 *= 0.5;
+        e2 -= 1;
+      }
+    }
+  }
+  r1 = z1 ? 0 : (x1 == 0.0 ? EXP_ZERO : e1);
+  r2 = z2 ? 0 : (x2 == 0.0 ? EXP_ZERO : e2);
+}
+
 // Cheap test "protect_update would return 1" from upper bounds of the norms;
 // protect_update is monotone in each argument (overflow.py:50-57), so a pass
 // here is exact.  A fail means "evaluate the exact norms".

@@ -245,8 +245,9 @@ __global__ void __launch_bounds__(NP * 64) k_diag_cplx_ws(Ctx c, DiagArgs a) {
           const double qx = sqrt(tx), qr = sqrt(tr);
           const double bl = (qx - qx * 0x1p-47) * p2(ex_), bh = (qx + qx * 0x1p-47) * p2(ex_);
           const double rl = (qr - qr * 0x1p-47) * p2(er_), rh = (qr + qr * 0x1p-47) * p2(er_);
-          e = protect_update_e(bl, rl, ax, omega);
-          full = e != protect_update_e(bh, rh, ax, omega);
+          int eh;
+          protect_update_e2(bl, rl, bh, rh, ax, omega, e, eh);
+          full = e != eh;
         } else {
           full = true;
         }
