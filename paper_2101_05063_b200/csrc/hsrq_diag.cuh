@@ -661,9 +661,8 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
           const double qx = sqrt(tx), qr = sqrt(tr);
           const double bl = (qx - qx * 0x1p-47) * p2(ex), bh = (qx + qx * 0x1p-47) * p2(ex);
           const double rl = (qr - qr * 0x1p-47) * p2(er), rh = (qr + qr * 0x1p-47) * p2(er);
-          int eh;
-          protect_update_e2(bl, rl, bh, rh, ax, omega, e, eh);
-          full = e != eh;
+          e = protect_update_e(bl, rl, ax, omega);
+          full = e != protect_update_e(bh, rh, ax, omega);
           if (full && pl == 0) HSRQ_COUNT(14);
         } else {
           full = true;

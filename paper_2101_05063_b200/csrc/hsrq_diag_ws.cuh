@@ -213,6 +213,8 @@ __global__ void __launch_bounds__(NP * 64) k_diag_cplx_ws(Ctx c, DiagArgs a) {
       const cplx ccj = mk(cr, -ci), svc = mk(sv, 0.0);
       const int ex_ = ilogb_pos(xb), er_ = ilogb_pos(rb);
       const double sx = p2(-max(-1000, min(1020, ex_))), sr = p2(-max(-1000, min(1020, er_)));
+      // |x_kp| for the certification, issued ahead of the row pass
+      const double ax = exact2 ? cabs_(xk) : 0.0;
       double tx = 0.0, tr = 0.0;
 #pragma unroll 1
       for (int i = pl + DP * role; i < kp; i += 2 * DP) {
@@ -239,7 +241,6 @@ __global__ void __launch_bounds__(NP * 64) k_diag_cplx_ws(Ctx c, DiagArgs a) {
       bool full = false;
       int e = 0;
       if (exact2) {
-        const double ax = cabs_(xk);
         if (ex_ > -1000 && ex_ < 1020 && er_ > -1000 && er_ < 1020 && tx >= 0x1p-960 &&
             tr >= 0x1p-960 && tx <= 16.0 && tr <= 16.0) {
           const double qx = sqrt(tx), qr = sqrt(tr);
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(NP * 64) k_diag_cplx_ws(Ctx c, DiagArgs a) {
         const double r0 = E2(2, 0), r1 = E2(2, 1), b0 = E2(3, 0), b1 = E2(3, 1);
         rm = r1 > r0 ? r1 : r0;
         bm = b1 > b0 ? b1 : b0;
-        if (full) e = protect_update_e(bm, rm, cabs_(xk), omega);
+        if (full) e = protect_update_e(bm, rm, ax, omega);
       }
       const bool g2 = exact2 && e < 0;
       if (__any_sync(FULL, g2)) {
