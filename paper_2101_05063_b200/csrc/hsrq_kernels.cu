@@ -1230,6 +1230,7 @@ int64_t host_enqueue(const double* H, int64_t ldh, int64_t n, int32_t b_r, const
     ldbd = n;
   }
   HostFeed feed{H, ldh, X, ldx, copy, evs.data(), d2h, 0, early, early ? 1 : 4};
+  if (const char* e = getenv("HSRQ_HOST_CHUNKS")) feed.chunks = std::max(1, atoi(e));
   int32_t* segd = (int32_t*)(w + L.seg);
   int32_t* aexpd = (int32_t*)(w + L.aexp);
   double* normsd = (double*)(w + L.norms);
