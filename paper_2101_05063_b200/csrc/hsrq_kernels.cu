@@ -792,8 +792,9 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   // HSRQ_LOOKAHEAD=0/1 forces it off/on.
   // Measured (tools/shard_time.py, config-5 shards, ms per solve, off -> on):
   // 1 GPU 515 -> 514, 1/2 shard 291 -> 261, 1/4 175 -> 162, 1/8 116 -> 105.
-  // Off for a whole config-5 group, where it gains nothing and the panel's
-  // launch times (the roofline's denominator) would include the sweep.
+  // Off for a whole config-5 group: with the warp-pair sweep it gains 1.4 %
+  // there (485 -> 478 ms) but the panel's launch times (the roofline's
+  // denominator) would then include the concurrent sweep (panel 335 -> 433 ms).
   bool lookahead = c.ms <= 6000;
   if (const char* e = getenv("HSRQ_LOOKAHEAD")) lookahead = atoi(e) != 0;
   // Bop / SS are double-buffered by column parity: the lookahead sweep of
