@@ -318,6 +318,12 @@ const char* hsrq_hessenberg_last_error(void);
 /* Elementwise device evaluations for bit-level parity of the scalar helpers. */
 int64_t hsrq_protect_update_batch(const double* bnorm, const double* hnorm, const double* xnorm,
                                   double omega, int64_t count, double* out, void* stream);
+/* protect_update at two argument pairs sharing xnorm, evaluated side by side
+ * as the complex sweep's guard-2 certification does (protect_update_e2 in
+ * csrc/hsrq_device.cuh); each output equals hsrq_protect_update_batch's. */
+int64_t hsrq_protect_update_pair_batch(const double* b1, const double* h1, const double* b2,
+                                       const double* h2, const double* xnorm, double omega,
+                                       int64_t count, double* out1, double* out2, void* stream);
 int64_t hsrq_hypot_batch(const double* x, const double* y, int64_t count, double* out,
                          void* stream);
 

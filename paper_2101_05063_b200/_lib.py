@@ -64,6 +64,7 @@ SIGNATURES = {
     "hsrq_tile_backtransform": (
         _i64, [_i64, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _i32, _f64, _p]),
     "hsrq_protect_update_batch": (_i64, [_p, _p, _p, _f64, _i64, _p, _p]),
+    "hsrq_protect_update_pair_batch": (_i64, [_p, _p, _p, _p, _p, _f64, _i64, _p, _p, _p]),
     "hsrq_hypot_batch": (_i64, [_p, _p, _i64, _p, _p]),
     "hsrq_debug_counters": (_i64, [_p, _i32]),
     "hsrq_compact_encode": (_i64, [_i64, _i32, _p, _p, _p, _p, _p, _p]),

@@ -269,6 +269,17 @@ __global__ void k_protect_batch(const double* b, const double* h, const double* 
     out[t] = p2(e);
   }
 }
+__global__ void k_protect_pair_batch(const double* b1, const double* h1, const double* b2,
+                                     const double* h2, const double* x, double omega,
+                                     int64_t count, double* out1, double* out2) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < count) {
+    int e1, e2;
+    protect_update_e2(b1[t], h1[t], b2[t], h2[t], x[t], omega, e1, e2);
+    out1[t] = p2(e1);
+    out2[t] = p2(e2);
+  }
+}
 __global__ void k_compact_encode(int64_t count, int cplx, const double* c_re, const double* c_im,
                                  const double* s, double* t1, double* t2) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1426,6 +1437,15 @@ int64_t hsrq_protect_update_batch(const double* bnorm, const double* hnorm, cons
   if (count <= 0) return 0;
   k_protect_batch<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       bnorm, hnorm, xnorm, omega, count, out);
+  return ck(cudaGetLastError(), "launch") ? 0 : HSRQ_ERR_CUDA;
+}
+
+int64_t hsrq_protect_update_pair_batch(const double* b1, const double* h1, const double* b2,
+                                       const double* h2, const double* xnorm, double omega,
+                                       int64_t count, double* out1, double* out2, void* stream) {
+  if (count <= 0) return 0;
+  k_protect_pair_batch<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      b1, h1, b2, h2, xnorm, omega, count, out1, out2);
   return ck(cudaGetLastError(), "launch") ? 0 : HSRQ_ERR_CUDA;
 }
 

@@ -63,6 +63,48 @@ def test_device_protect_update_bitwise(dev):
     assert np.array_equal(out.cpu().numpy(), g["protect"])
 
 
+def test_device_protect_update_pair_bitwise(dev):
+    """protect_update_e2 (both guard-2 interval ends side by side, the
+    complex sweep's certification) equals protect_update at each pair: the
+    golden inputs paired with their neighbours' norms, and random pairs
+    straddling binade and overflow edges the way the certification builds
+    them (q (1 -/+ 2^-47) 2^e)."""
+    from oracle import oracle
+    from paper_2101_05063_b200 import _lib
+
+    g = golden("scalars")
+    omega = float(g["omega"])
+    rng = np.random.default_rng(7)
+    n = 4000
+    x = np.concatenate([g["px"], 10.0 ** rng.uniform(-300, 300, n), rng.uniform(0.0, 2.0, n)])
+    m = x.size
+    ex = rng.integers(-1000, 1000, m)
+    q = rng.uniform(0.5, 4.0, m)
+    b1 = np.concatenate([g["pb"], np.ldexp(q[g["pb"].size:] * (1 - 2.0 ** -47), ex[g["pb"].size:])])
+    b2 = np.concatenate([np.roll(g["pb"], 1), np.ldexp(q[g["pb"].size:] * (1 + 2.0 ** -47), ex[g["pb"].size:])])
+    er = rng.integers(-1000, 1000, m)
+    r = rng.uniform(0.5, 4.0, m)
+    h1 = np.concatenate([g["ph"], np.ldexp(r[g["ph"].size:] * (1 - 2.0 ** -47), er[g["ph"].size:])])
+    h2 = np.concatenate([np.roll(g["ph"], 1), np.ldexp(r[g["ph"].size:] * (1 + 2.0 ** -47), er[g["ph"].size:])])
+    # half of the random pairs scaled so that b + h x sits near omega
+    sel = np.arange(g["pb"].size, m, 2)
+    f = omega / np.maximum(b2[sel] + h2[sel] * x[sel], 1e-300)
+    for a in (b1, b2, h1, h2):
+        sc = a[sel] * f
+        a[sel] = np.where(np.isfinite(sc), sc, a[sel])
+    t = [_d(a, dev) for a in (b1, h1, b2, h2, x)]
+    o1, o2 = torch.empty_like(t[0]), torch.empty_like(t[0])
+    s = torch.cuda.current_stream().cuda_stream
+    assert _lib.load().hsrq_protect_update_pair_batch(*[_p(a) for a in t], omega, m, _p(o1), _p(o2),
+                                                      s) == 0
+    torch.cuda.synchronize()
+    w1 = np.array([oracle.protect_update(b1[i], h1[i], x[i], omega) for i in range(m)])
+    w2 = np.array([oracle.protect_update(b2[i], h2[i], x[i], omega) for i in range(m)])
+    assert np.array_equal(o1.cpu().numpy(), w1)
+    assert np.array_equal(o2.cpu().numpy(), w2)
+    assert (w1 < 1.0).sum() > 100 and (w1 != w2).sum() > 0  # the cases are not all trivial
+
+
 def _tile_diag(dev, k, b, hd, hl, has_left, lre, lim, rright, xin, omega):
     from paper_2101_05063_b200 import _lib
 
