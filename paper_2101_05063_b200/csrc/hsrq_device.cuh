@@ -18,6 +18,35 @@ namespace hsrq {
 
 constexpr int EXP_ZERO = -1075;  // exponent of a scale that halved to 0
 
+// Schedule fuzzing (race check; compute-sanitizer is not available on the GPU
+// pool).  The diagnostics build `-DHSRQ_FUZZ` (libhsrq_b200_fuzz.so,
+// tools/race_fuzz.py) makes a pseudo-random subset of threads sleep up to
+// ~2 us right after every warp / pair / CTA barrier of the diagonal sweeps,
+// the panel and k_scalars, so a shared-memory value read without the barrier
+// that orders it behind its write (or overwritten before its last reader is
+// done) changes the result, which the fuzz run then compares bitwise with
+// the production build.  The production build compiles these to plain barriers.
+#ifdef HSRQ_FUZZ
+// bit per source file (HSRQ_FUZZ_FILE at the point of use): 1 hsrq_diag.cuh,
+// 2 hsrq_diag_ws.cuh, 4 hsrq_panel.cuh, 8 hsrq_henry.cuh; HSRQ_FUZZ_MASK
+// (environment, read at the first solve) selects which files are fuzzed
+__device__ unsigned g_fuzz_mask = 0xffffffffu;
+__device__ __forceinline__ void fuzz_delay(unsigned site) {
+  if (!(g_fuzz_mask & (site >> 16))) return;
+  unsigned h = (blockIdx.x * 0x9E3779B1u) ^ (threadIdx.x * 0x85EBCA77u) ^ (site * 0xC2B2AE3Du) ^
+               (unsigned)clock();
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  if ((h & 3u) == 0u) __nanosleep((h >> 16) & 2047u);
+}
+#define HSRQ_SYNCWARP() (__syncwarp(), ::hsrq::fuzz_delay(__LINE__ | (HSRQ_FUZZ_FILE << 16)))
+#define HSRQ_SYNCTHREADS() (__syncthreads(), ::hsrq::fuzz_delay(__LINE__ | (HSRQ_FUZZ_FILE << 16)))
+#else
+#define HSRQ_SYNCWARP() __syncwarp()
+#define HSRQ_SYNCTHREADS() __syncthreads()
+#endif
+
 struct cplx {
   double re, im;
 };

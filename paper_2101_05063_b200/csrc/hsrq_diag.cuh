@@ -19,6 +19,8 @@
 
 // Lanes per shift (DP) and warps per CTA are template parameters; the host
 // picks the variant (see diag_launch in hsrq_kernels.cu).
+#undef HSRQ_FUZZ_FILE
+#define HSRQ_FUZZ_FILE 1u
 constexpr double DSLACK = 1.0 + 0x1p-46;
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -141,7 +143,7 @@ __device__ __forceinline__ void load_hmax(const Ctx& c, const DiagArgs& a, doubl
     }
     hmax[kp] = m;
   }
-  __syncthreads();
+  HSRQ_SYNCTHREADS();
 }
 
 __device__ __forceinline__ void put_rot(const Ctx& c, const DiagArgs& a, int64_t q, int row,
@@ -171,6 +173,9 @@ __device__ __forceinline__ void diag_real_tail(const Ctx& c, const DiagArgs& a, 
 #define XX(i) Xs[(i) * DG + grp]
   const double v0 = VV(0);
   double x0 = XX(0);
+  // every lane has read row 0 before lane 0 may rescale / overwrite it below
+  // (found by the schedule-fuzzing race check, tools/race_fuzz.py)
+  HSRQ_SYNCWARP();
   double c0 = 1.0, s0 = 0.0, piv = v0;
   double hleft0 = 0.0;
   if (a.has_left) {
@@ -201,7 +206,7 @@ __device__ __forceinline__ void diag_real_tail(const Ctx& c, const DiagArgs& a, 
   }
   x0 = x0 / piv;
   if (pl == 0) XX(0) = x0;
-  __syncwarp();
+  HSRQ_SYNCWARP();
   // (no early return: dead or padding groups keep executing so that warp
   // shuffles stay convergent; their writes are masked by `live`)
   if (live) {
@@ -262,7 +267,7 @@ __device__ __forceinline__ void diag_real_tail(const Ctx& c, const DiagArgs& a, 
     lc = nc;
     ls = ns;
   }
-  __syncwarp();
+  HSRQ_SYNCWARP();
   double zm = 0.0;
   for (int i = pl; i < k - 1; i += DP) {
     const double z = fabs(VV(i));
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_real(Ctx c, DiagArgs a) {
     fill_col(c, a, hb, k - 2, k, lane);
     cp_wait<0>();
   }
-  __syncwarp();
+  HSRQ_SYNCWARP();
   int gexp = 0;
   for (int kp = k - 1; kp >= 1; --kp) {
     const double* hcol = hb + cur * MAXK;  // column kp-1, rows 0..kp
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_real(Ctx c, DiagArgs a) {
     xm = nxm;
     vm = nvm;
     cp_wait<0>();
-    __syncwarp();
+    HSRQ_SYNCWARP();
     cur ^= 1;
   }
   diag_real_tail<DP>(c, a, q, col, live, pl, grp, k, V, Xs, gexp, robust);
@@ -485,7 +490,7 @@ __device__ __forceinline__ void diag_cplx_operands(const Ctx& c, const DiagArgs&
     lci = nci;
     ls = ns;
   }
-  __syncwarp();
+  HSRQ_SYNCWARP();
   double zm = 0.0;
   for (int i = pl; i < k - 1; i += DP) {
     const double z = cabs_(mk(Vr[IX(i)], Vi[IX(i)]));
@@ -571,7 +576,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
     fill_col(c, a, hb, k - 2, k, lane);
     cp_wait<0>();
   }
-  __syncwarp();
+  HSRQ_SYNCWARP();
   int gexp = 0;
   for (int kp = k - 1; kp >= 1; --kp) {
     const double* hcol = hb + cur * MAXK;  // column kp-1, rows 0..kp
@@ -738,12 +743,13 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
     xb = nxb;
     vb = nvb;
     cp_wait<0>();
-    __syncwarp();
+    HSRQ_SYNCWARP();
     cur ^= 1;
   }
   // j = 0: cross-tile rotation (creduce_diag :449-463) and R[0,0] (:546-550)
   const cplx v0 = mk(Vr[IX(0)], Vi[IX(0)]);
   cplx x0 = mk(Xr[IX(0)], Xi[IX(0)]);
+  HSRQ_SYNCWARP();  // row 0 read by every lane before lane 0 rescales / overwrites it
   double c0r = 1.0, c0i = 0.0, s0 = 0.0;
   cplx d = v0;
   if (a.has_left) {
@@ -783,7 +789,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
     Xr[IX(0)] = x0.re;
     Xi[IX(0)] = x0.im;
   }
-  __syncwarp();
+  HSRQ_SYNCWARP();
   if (live) {
     for (int i = pl; i < k; i += DP) {
       if (a.tile_mode) {

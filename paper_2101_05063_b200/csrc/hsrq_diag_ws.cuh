@@ -21,8 +21,13 @@
 // triple-buffered: the chain warp prefetches column kp-2 while the bulk warp
 // still reads column kp.
 
+#undef HSRQ_FUZZ_FILE
+#define HSRQ_FUZZ_FILE 2u
 __device__ __forceinline__ void pair_sync(int id) {
   asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory");
+#ifdef HSRQ_FUZZ
+  fuzz_delay((unsigned)id | (HSRQ_FUZZ_FILE << 16));
+#endif
 }
 
 template <int DP, int NP>
@@ -108,7 +113,7 @@ __global__ void __launch_bounds__(NP * 64) k_diag_cplx_ws(Ctx c, DiagArgs a) {
       } else {
         cp_wait<0>();
       }
-      __syncwarp();
+      HSRQ_SYNCWARP();
       const double* hcol = HB(kp - 1);
       const cplx vk = mk(Vr[IX(kp)], Vi[IX(kp)]);
       const cplx xk = mk(Xr[IX(kp)], Xi[IX(kp)]);
@@ -309,7 +314,7 @@ __global__ void __launch_bounds__(NP * 64) k_diag_cplx_ws(Ctx c, DiagArgs a) {
         Xr[IX(i)] = x.re;
         Xi[IX(i)] = x.im;
       }
-      __syncwarp();
+      HSRQ_SYNCWARP();
     } else {
       bxk = xk;
       bcr = cr;
@@ -322,6 +327,7 @@ __global__ void __launch_bounds__(NP * 64) k_diag_cplx_ws(Ctx c, DiagArgs a) {
   // j = 0: cross-tile rotation (creduce_diag :449-463) and R[0,0] (:546-550)
   const cplx v0 = mk(Vr[IX(0)], Vi[IX(0)]);
   cplx x0 = mk(Xr[IX(0)], Xi[IX(0)]);
+  HSRQ_SYNCWARP();  // row 0 read by every lane before lane 0 rescales / overwrites it
   double c0r = 1.0, c0i = 0.0, s0 = 0.0;
   cplx d = v0;
   if (a.has_left) {
@@ -361,7 +367,7 @@ __global__ void __launch_bounds__(NP * 64) k_diag_cplx_ws(Ctx c, DiagArgs a) {
     Xr[IX(0)] = x0.re;
     Xi[IX(0)] = x0.im;
   }
-  __syncwarp();
+  HSRQ_SYNCWARP();
   if (live) {
     for (int i = pl; i < k; i += DP) {
       if (a.tile_mode) {
@@ -462,7 +468,7 @@ __global__ void __launch_bounds__(NP * 64) k_diag_real_ws(Ctx c, DiagArgs a) {
       } else {
         cp_wait<0>();
       }
-      __syncwarp();
+      HSRQ_SYNCWARP();
       const double* hcol = HB(kp - 1);
       const double vk = VV(kp);
       double xk = XX(kp);
@@ -555,7 +561,7 @@ __global__ void __launch_bounds__(NP * 64) k_diag_real_ws(Ctx c, DiagArgs a) {
         XX(i) = (xx - (cc * xk) * vv) + (ss * xk) * hd;
         VV(i) = cc * hd + ss * vv;
       }
-      __syncwarp();
+      HSRQ_SYNCWARP();
     } else {
       bcc = cc;
       bss = ss;

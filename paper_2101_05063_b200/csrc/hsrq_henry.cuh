@@ -20,6 +20,8 @@
 // rows are loaded coalesced, their values broadcast lane by lane, and every
 // lane runs the same scalar recurrence; lane j keeps output row base + j.
 
+#undef HSRQ_FUZZ_FILE
+#define HSRQ_FUZZ_FILE 8u
 constexpr int HENRY_THREADS = 512;
 
 struct HenryArgs {
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(HENRY_THREADS) k_henry_real(HenryArgs a) {
       cs[0] = 0.0;
       a.status[q] = 0;
     }
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
     int p = 0;
     bool ok = true;
     for (int64_t kp = n - 1; kp >= 1; --kp) {
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(HENRY_THREADS) k_henry_real(HenryArgs a) {
         piv[p ^ 1][0] = c * hdl + s * vi;
       }
       p ^= 1;
-      __syncthreads();
+      HSRQ_SYNCTHREADS();
     }
     if (ok) {
       const double v0 = piv[p][0];
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(HENRY_THREADS) k_henry_real(HenryArgs a) {
         x[0] = piv[p][1] / v0;
       }
     }
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
     if (ok && tid < 32) {  // backtransform (numba_backend.py:314-323)
       double t1 = x[0];
       for (int64_t base = 0; base < n - 1; base += 32) {
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(HENRY_THREADS) k_henry_real(HenryArgs a) {
       }
       if (lane == 0) x[n - 1] = t1;
     }
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
   }
 }
 
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(HENRY_THREADS) k_henry_cplx(HenryArgs a) {
       cs[0] = 0.0;
       a.status[q] = 0;
     }
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
     int p = 0;
     bool ok = true;
     for (int64_t kp = n - 1; kp >= 1; --kp) {
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(HENRY_THREADS) k_henry_cplx(HenryArgs a) {
         piv[p ^ 1][3] = xn.im;
       }
       p ^= 1;
-      __syncthreads();
+      HSRQ_SYNCTHREADS();
     }
     if (ok) {
       const cplx v0 = mk(piv[p][0], piv[p][1]);
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(HENRY_THREADS) k_henry_cplx(HenryArgs a) {
         x[0] = make_double2(x0.re, x0.im);
       }
     }
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
     if (ok && tid < 32) {  // rotation sweep of henry_solve_complex (:915-923)
       const double2 x0 = x[0];
       cplx t1 = mk(x0.x, x0.y);
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(HENRY_THREADS) k_henry_cplx(HenryArgs a) {
       }
       if (lane == 0) x[n - 1] = make_double2(t1.re, t1.im);
     }
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
   }
 }
 

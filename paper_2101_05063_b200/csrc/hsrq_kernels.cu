@@ -420,6 +420,12 @@ size_t diag_smem() {
 bool diag_attrs() {
   static bool done = false;
   if (done) return true;
+#ifdef HSRQ_FUZZ
+  if (const char* m = getenv("HSRQ_FUZZ_MASK")) {
+    const unsigned v = (unsigned)strtoul(m, nullptr, 0);
+    cudaMemcpyToSymbol(g_fuzz_mask, &v, sizeof(v));
+  }
+#endif
   const char* pf = getenv("HSRQ_PANEL_FAST");
   if (pf) g_panel_fast = atoi(pf);
   const char* pp = getenv("HSRQ_PANEL_PREFETCH");

@@ -20,6 +20,8 @@
 // CTA owns whole tile rows, so step 3 -- which needs the GEMM result -- is
 // CTA-local in the epilogue.
 
+#undef HSRQ_FUZZ_FILE
+#define HSRQ_FUZZ_FILE 4u
 #ifndef SCAL_MINB
 #define SCAL_MINB 6  // k_scalars: 6 CTAs per SM (80 registers): 28.7 -> 27.6 ms at config 5
 #endif
@@ -565,7 +567,7 @@ __device__ __forceinline__ void epilogue_b128(const Ctx& c, const PanelArgs& p, 
     sm.red[1][0][cl0 + 1] = dkey(mr1);
   }
   tl_mark(tlp, 6);
-  __syncthreads();
+  HSRQ_SYNCTHREADS();
   // ---- step 3 guard (:287-301), one thread per column ----
   int my_need = 0;
   if (tid < BN) {
@@ -613,12 +615,12 @@ __device__ __forceinline__ void epilogue_b128(const Ctx& c, const PanelArgs& p, 
       hb = fmax(hb, __shfl_xor_sync(0xffffffffu, hb, o));
       hr = fmax(hr, __shfl_xor_sync(0xffffffffu, hr, o));
     }
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
     if (rp == 0 && cplx) {
       sm.red[0][0][cl0] = dkey(hb);
       sm.red[1][0][cl0] = dkey(hr);
     }
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
     if (tid < BN && sm.need[0][tid]) {
       const int cc = tid, ccr = cc & ~1;
       const double zr = sm.z3r[0][cc], zi = sm.z3i[0][cc];
@@ -632,7 +634,7 @@ __device__ __forceinline__ void epilogue_b128(const Ctx& c, const PanelArgs& p, 
         sm.z3i[0][cc] = zi * x3;
       }
     }
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
   }
   tl_mark(tlp, 7);
   // ---- pass 2: X''' = x3 X'' - Cr_old zk ; Cr_new = A W + P Cr_old - c0 lambda e_{js-1} ----
@@ -808,7 +810,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
 
   for (int kc = 0; kc < (c.diag_gemm_only == 2 ? 0 : nk); kc++) {
     cp_wait<STAGES - 2>();
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
     {
       int nxt = kc + STAGES - 1;
       if (nxt < nk) {
@@ -838,7 +840,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
     }
   }
   cp_wait<0>();
-  __syncthreads();
+  HSRQ_SYNCTHREADS();
   if (tl_) {
     unsigned long long g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -859,7 +861,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
       sm.u.C[cc][r + 8] = acc[mi][ni][2];
       sm.u.C[cc + 1][r + 8] = acc[mi][ni][3];
     }
-  __syncthreads();
+  HSRQ_SYNCTHREADS();
 
   if (FAST) {  // b_r == 128: one full tile row per CTA, a single guard segment
 #ifdef HSRQ_TIMELINE_EPI
@@ -965,7 +967,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
       seg_max2<true>(sm, 1, seg, cl0, mr0, mr1, rp);
     }
   }
-  __syncthreads();
+  HSRQ_SYNCTHREADS();
   if (tl_) {
     unsigned long long g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -1006,7 +1008,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
   if (__syncthreads_or(my_need)) {  // rare: exact hypot maxima for flagged complex columns
     if (tid == 0) HSRQ_COUNT(11);
     for (int e = tid; e < 2 * SMAX * BN; e += PANEL_THREADS) (&sm.red[0][0][0])[e] = 0ULL;
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
     if (cplx && v0) {
 #pragma unroll
       for (int j = 0; j < EP_RPT; j++) {
@@ -1018,7 +1020,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
         }
       }
     }
-    __syncthreads();
+    HSRQ_SYNCTHREADS();
     for (int e = tid; e < SMAX * BN; e += PANEL_THREADS) {
       const int sg = e / BN, cc = e % BN;
       if (!sm.need[sg][cc]) continue;
@@ -1036,7 +1038,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
     }
   }
   for (int e = tid; e < SMAX * BN; e += PANEL_THREADS) (&sm.red[0][0][0])[e] = 0ULL;
-  __syncthreads();
+  HSRQ_SYNCTHREADS();
   if (tl_) {
     unsigned long long g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -1114,7 +1116,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
     }
     if (SEG16 && seg < ntiles) seg_max2<true>(sm, 0, seg, cl0, mb0, mb1, rp);
   }
-  __syncthreads();
+  HSRQ_SYNCTHREADS();
   // new beta and the step-1 bound for the next tile column
   for (int e = tid; e < SMAX * BN; e += PANEL_THREADS) {
     const int sg = e / BN, cc = e % BN;
