@@ -93,7 +93,9 @@ size_t hsrq_workspace_bytes(int64_t n, int32_t b_r, int64_t m_cplx, int64_t m_re
  *           (ldb); b_broadcast = 1 -> one real n-vector used for every
  *           column (imaginary parts 0), the start vector _iterate repeats
  *           (inviter.py:127-133)
- *  X        out, n x ncol column-major (ldx); may alias B when ldb == ldx
+ *  X        out, n x ncol column-major (ldx; this build requires ldx == n,
+ *           the in-place crossover block shares X's layout); may alias B
+ *           when ldb == ldx
  *  c_re, c_im, s   out, recorded rotations, n x (m_cplx + m_real) column-major
  *           (ldc), row j mixing columns j-1 and j (GivensTable, core.py:168-179);
  *           c_im is written as 0 for real shifts

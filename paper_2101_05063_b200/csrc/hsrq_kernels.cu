@@ -34,6 +34,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "../../include/hsrq.h"
 #include "hsrq_device.cuh"
@@ -417,9 +418,25 @@ size_t diag_smem() {
 #define HSRQ_DIAG_REAL(X) X(2, 2) X(4, 2) X(4, 4) X(4, 8) X(8, 6) X(16, 8) X(32, 8) X(16, 16) X(32, 16)
 #define HSRQ_DIAG_CPLX(X) X(2, 1) X(4, 1) X(4, 2) X(4, 4) X(8, 4) X(16, 8) X(32, 8) X(16, 16) X(32, 16)
 
+// Function attributes (raised dynamic shared-memory limits) and __device__
+// symbols are per device: the one-shot setup below runs once per device
+// ordinal, under a mutex (a process may drive several GPUs from several
+// host threads).
+constexpr int MAX_DEVICES = 64;
+std::mutex g_setup_mu;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
 bool diag_attrs() {
-  static bool done = false;
-  if (done) return true;
+  static bool done[MAX_DEVICES] = {};
+  const int dev = current_device();
+  if (dev < 0 || dev >= MAX_DEVICES) return false;
+  std::lock_guard<std::mutex> lock(g_setup_mu);
+  if (done[dev]) return true;
 #ifdef HSRQ_FUZZ
   if (const char* m = getenv("HSRQ_FUZZ_MASK")) {
     const unsigned v = (unsigned)strtoul(m, nullptr, 0);
@@ -468,8 +485,8 @@ bool diag_attrs() {
 #undef HSRQ_ATTR_W
   if (const char* w = getenv("HSRQ_DIAG_WS")) g_diag_ws = atoi(w);
   if (const char* w = getenv("HSRQ_DIAG_WSR")) g_diag_ws_r = atoi(w);
-  done = ok;
-  return done;
+  done[dev] = ok;
+  return ok;
 }
 
 // Automatic choice: lanes per shift so that count * DP / 32 warps roughly
@@ -694,10 +711,14 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     return HSRQ_ERR_CONFIG;
   }
 
-  static bool attr_done = false;
+  static bool attr_done[MAX_DEVICES] = {};
   const size_t panel_smem = sizeof(PanelSmem);
-  if (!attr_done) {
-    if (!diag_attrs() ||
+  const int cur_dev = current_device();
+  if (cur_dev < 0 || cur_dev >= MAX_DEVICES) return HSRQ_ERR_CONFIG;
+  if (!diag_attrs()) return HSRQ_ERR_CUDA;
+  std::unique_lock<std::mutex> setup_lock(g_setup_mu);
+  if (!attr_done[cur_dev]) {
+    if (
         !ck(cudaFuncSetAttribute(k_panel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)panel_smem), "attr panel") ||
         !ck(cudaFuncSetAttribute(k_panel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -709,8 +730,9 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
         !ck(cudaFuncSetAttribute(k_panel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)panel_smem), "attr panel fast"))
       return HSRQ_ERR_CUDA;
-    attr_done = true;
+    attr_done[cur_dev] = true;
   }
+  setup_lock.unlock();
   // Optional per-launch timing: events around every launch, one sync at the end.
   const int nev = 6 * c.N + 6;
   cudaEvent_t* ev = nullptr;
