@@ -239,21 +239,22 @@ def run_gpu(args):
         r = gs.launch(start, True, robust=True, mode="eigvec", stream=stream, sync=False)
         return r
 
-    gather_bufs = None
+    gather_out = None
     if world > 1:
-        cols = [None] * world
+        from paper_2101_05063_b200.parallel import gather_columns
+
         counts = torch.tensor([gs.ncol], device=dev)
         allc = [torch.zeros_like(counts) for _ in range(world)]
         dist.all_gather(allc, counts)
-        maxc = int(max(int(c.item()) for c in allc))
-        gather_bufs = [torch.empty((maxc, n), dtype=torch.float64, device=dev) for _ in range(world)] if rank == 0 else None
-        send = torch.zeros((maxc, n), dtype=torch.float64, device=dev)
+        counts = [int(c.item()) for c in allc]
+        gather_out = torch.empty((sum(counts), n), dtype=torch.float64, device=dev) if rank == 0 else None
 
     def gather():
+        # parallel.gather_columns: every rank's X block to rank 0 over NCCL
+        # send/recv, exactly X's bytes once (what hsrq3in_distributed uses)
         if world == 1:
             return
-        send[: gs.ncol].copy_(gs.X)
-        dist.gather(send, gather_bufs if rank == 0 else None, dst=0)
+        gather_columns(gs.X, counts, dst=0, out=gather_out)
 
     for _ in range(args.warmup):
         step()
@@ -356,6 +357,40 @@ def run_gpu(args):
             out.nfail == int(nf) and np.array_equal(out.X, gs.X.cpu().numpy())
             and np.array_equal(out.seg_exp, gs.seg_exp.cpu().numpy()))
 
+    # ---- e2e through the drop-in Python API: hsrq3in(H, eigenvalues) with a
+    # numpy H and numpy eigenvalues (caller order), numpy eigenvectors out --
+    # exactly what a caller of the reference's entry point (inviter.py:186-254)
+    # pays: H upload + checks, the solve, the caller-order result assembly ----
+    e2e_api = None
+    if not args.no_e2e and world == 1:
+        import time as _time
+
+        from paper_2101_05063_b200 import InviterConfig, hsrq3in
+
+        sel_api = np.concatenate([ec, er.astype(np.complex128)])
+        sel_api = sel_api[np.random.default_rng(0).permutation(sel_api.size)]
+        cfg_api = InviterConfig(b_r=b_r, max_restarts=0)
+        hf = np.asfortranarray(h)
+        r_api = hsrq3in(hf, sel_api, cfg_api)  # warm-up
+        conv_api = int(r_api.converged.sum())
+        del r_api
+        wall = []
+        for _ in range(max(1, args.steps)):
+            torch.cuda.synchronize()
+            t0 = _time.perf_counter()
+            r_api = hsrq3in(hf, sel_api, cfg_api)
+            wall.append(_time.perf_counter() - t0)
+            host_ms = r_api.extras.get("host_ms")
+            del r_api
+        ams = 1e3 * float(np.mean(wall))
+        e2e_api = {"value": sel_api.size / (ams / 1e3), "unit": "eigenvectors/s", "ms_per_step": ams,
+                   "h2d_bytes_per_step": int(h.nbytes + sel_api.nbytes),
+                   "d2h_bytes_per_step": int(n * sel_api.size * 16),
+                   "api": "hsrq3in(H: numpy float64 (n, n) F-order, eigenvalues: numpy complex128 "
+                          "in mixed caller order) -> EigvecResult with numpy (n, m) complex128 "
+                          "vectors; one attempt (max_restarts=0); host wall clock",
+                   "converged": conv_api, "last_call_ms": host_ms}
+
     # ---- correctness on this rank's shard: convergence of every column and the
     # north_star residual bound on a sample (the last step's X is the result) ----
     norms_all = gs.norms.cpu().numpy()
@@ -440,6 +475,8 @@ def run_gpu(args):
     }
     if e2e:
         line["e2e"] = e2e
+    if e2e_api:
+        line["e2e_api"] = e2e_api
     if world == 1 and not args.no_shards:
         line["shard_projection"] = shard_projection(dh, b_r, er, ec, start, stream)
     if world == 1 and not args.no_cpu:

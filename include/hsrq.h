@@ -27,6 +27,10 @@
  *                      z = Q0 x: the front end
  *   hsrq_protect_update_batch   protect_update, _kernels/numba_backend.py:47-67
  *   hsrq_hypot_batch            libm hypot as bound by numba (every rotation)
+ *   hsrq_h_upload / hsrq_pack_download
+ *                      the host side of dhsrq3in / chsrq3in / hsrq3in
+ *                      (inviter.py:155-254): HessenbergMatrix's copy and
+ *                      checks (core.py:60-98) and the result assembly
  *   hsrq_tile_diag              reduce_diag + solve_rsolve (numba_backend.py:
  *                               75-106, 133-195) and creduce_diag +
  *                               csolve_crsolve (:420-464, :554-576) on one
@@ -316,6 +320,40 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
 int64_t hsrq_backmultiply(const double* Q, int64_t ldq, int64_t n, const double* X, int64_t ldx,
                           int64_t ncol, double* Z, int64_t ldz, void* stream);
 const char* hsrq_hessenberg_last_error(void);
+
+/*
+ * Host I/O of the drop-in API (csrc/hsrq_hostio.cuh): what hsrq3in /
+ * dhsrq3in / chsrq3in (inviter.py:155-254) pay around the solve when called
+ * with numpy arrays.  Both stage through a process-wide pinned ring filled /
+ * drained by host worker threads; `*_host` pointers are pageable memory.
+ *
+ * hsrq_h_upload: H from the caller's array (order 1 = column-major /
+ *   Fortran, 0 = row-major / C: transposed on the device) into the
+ *   column-major device H (ldh >= n).  checks_host[3] receives what
+ *   HessenbergMatrix (core.py:60-98) computes on the host: [0] the infinity
+ *   norm, bit-identical to np.max(np.sum(np.abs(F-order H), axis=1)) (numpy
+ *   sums a Fortran array's rows left to right), [1] the number of nonzeros
+ *   below the first subdiagonal (the ConfigError check, core.py:70-73),
+ *   [2] the number of zero subdiagonal entries (is_unreduced, core.py:86-91).
+ *   `stream` waits for the upload.  Returns 0 or a negative HSRQ_ERR_*.
+ *
+ * hsrq_pack_download: the solve's columns -> the caller's (n, m) C-order
+ *   result (EigvecResult.vectors, inviter.py:53-59): out[i, j] =
+ *   X[re_col[j]][i] + 1j * im_sign[j] * X[im_col[j]][i] (cplx_out = 1,
+ *   complex128; im_col[j] < 0: real column) or X[re_col[j]][i]
+ *   (cplx_out = 0, float64), X column-major n x ncol (ldx).  Column maps are
+ *   host arrays of m entries.  Packs row blocks on the device after the work
+ *   queued on `stream` and returns once out_host is written.
+ */
+int64_t hsrq_h_upload(const double* h_host, int32_t order, int64_t n, double* H, int64_t ldh,
+                      double* checks_host, void* stream);
+/* hsrq_host_prefault: take the first-touch page faults of a fresh host
+ * buffer (e.g. the numpy result hsrq_pack_download will fill) on `threads`
+ * threads -- meant to run while the device solves.  Returns 0. */
+int64_t hsrq_host_prefault(void* ptr, int64_t bytes, int32_t threads);
+int64_t hsrq_pack_download(const double* X, int64_t ldx, int64_t n, int64_t m,
+                           const int64_t* re_col, const int64_t* im_col, const double* im_sign,
+                           int32_t cplx_out, void* out_host, void* stream);
 
 /* Elementwise device evaluations for bit-level parity of the scalar helpers. */
 int64_t hsrq_protect_update_batch(const double* bnorm, const double* hnorm, const double* xnorm,

@@ -1559,3 +1559,5 @@ int64_t hsrq_compact_decode(int64_t count, int32_t cplx, const double* t1, const
 }
 
 }  // extern "C"
+
+#include "hsrq_hostio.cuh"

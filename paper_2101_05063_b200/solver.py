@@ -41,18 +41,97 @@ def default_device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+HOST_CHECK_MAX_N = 2048  # structure check on the host up to this n (cheap), else on the device
+
+
+class HostHessenberg:
+    """The caller's array before upload, with the checks that need no device:
+    shape / dtype (core.py:66-69), the structure check for n <= 2048
+    (core.py:70-73; larger matrices are checked by hsrq_h_upload on the
+    device, same boolean), and is_unreduced (core.py:86-91, the subdiagonal
+    only).  No copy unless the dtype or the memory layout requires one."""
+
+    def __init__(self, h):
+        a = np.asarray(h)
+        if a.dtype != np.float64:
+            a = np.array(a, dtype=np.float64, order="F")
+        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+            raise ConfigError(f"expected a square matrix, got shape {a.shape}")
+        if not (a.flags.c_contiguous or a.flags.f_contiguous):
+            a = np.asfortranarray(a)
+        n = a.shape[0]
+        if 3 <= n <= HOST_CHECK_MAX_N:
+            low = a[2:, :-2]
+            if np.any(low[np.tril_indices(n - 2)] != 0.0):
+                raise ConfigError("matrix has nonzeros below the first subdiagonal")
+        self.a = a
+        self.n = n
+        self.unreduced = bool(n == 1 or np.all(a[np.arange(1, n), np.arange(0, n - 1)] != 0.0))
+
+    def is_unreduced(self):
+        return self.unreduced
+
+
 class DeviceHessenberg:
-    """H resident in HBM, column-major with an even leading dimension."""
+    """H resident in HBM, column-major with an even leading dimension.
+
+    ``norm_inf`` / ``unreduced`` are HessenbergMatrix.infinity_norm() /
+    is_unreduced() (core.py:80-93), bit for bit."""
 
     def __init__(self, h, device=None):
         hm = h if isinstance(h, HessenbergMatrix) else HessenbergMatrix(h)
         self.n = hm.n
         self.device = device or default_device()
         self.ldh = self.n + (self.n & 1)
-        t = torch.zeros((self.n, self.ldh), dtype=torch.float64)
-        # row j of t = column j of H (column-major storage)
-        t[:, : self.n] = torch.from_numpy(np.array(hm.data.T, order="C"))
-        self.t = t.to(self.device, non_blocking=False)
+        self.t = torch.zeros((self.n, self.ldh), dtype=torch.float64, device=self.device)
+        self._upload(hm.data)
+        self.norm_inf = hm.infinity_norm()
+        self.unreduced = hm.is_unreduced()
+
+    def _upload(self, a):
+        """hsrq_h_upload: pinned-ring staged copy (+ device transpose of a
+        C-order array) and the structure / norm checks; returns the checks."""
+        lib = _lib.load()
+        order = 1 if a.flags.f_contiguous else 0
+        chk = np.zeros(3)
+        st = torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            r = lib.hsrq_h_upload(ctypes.c_void_p(a.ctypes.data), order, self.n, _ptr(self.t),
+                                  self.ldh, ctypes.c_void_p(chk.ctypes.data),
+                                  ctypes.c_void_p(st.cuda_stream))
+        if r < 0:
+            raise RuntimeError(f"hsrq_h_upload failed ({r}): {_lib.last_error()}")
+        return chk
+
+    @classmethod
+    def upload(cls, h, device=None):
+        """Validate and upload a caller's array the way HessenbergMatrix(h)
+        does (core.py:66-77: float64, square, zero below the subdiagonal --
+        the same ConfigError messages), without the host-side F-order copy:
+        the array goes to the device as it lies in memory and the structure
+        check and the infinity norm (the reference's left-to-right row sums
+        of its F-order copy) run on the device, exactly."""
+        hv = h if isinstance(h, HostHessenberg) else HostHessenberg(h)
+        a = hv.a
+        self = cls.__new__(cls)
+        self.n = a.shape[0]
+        self.device = device or default_device()
+        self.ldh = self.n + (self.n & 1)
+        self.t = torch.empty((self.n, self.ldh), dtype=torch.float64, device=self.device)
+        if self.ldh != self.n:
+            self.t[:, self.n:].zero_()
+        chk = self._upload(a)
+        if self.n >= 3 and chk[1] != 0:
+            raise ConfigError("matrix has nonzeros below the first subdiagonal")
+        self.norm_inf = float(chk[0])
+        self.unreduced = bool(self.n == 1 or chk[2] == 0)
+        return self
+
+    def infinity_norm(self):
+        return self.norm_inf
+
+    def is_unreduced(self):
+        return self.unreduced
 
     @classmethod
     def of(cls, h, device=None):
@@ -85,6 +164,7 @@ class GroupOutput:
     mr: int
     launches: int
     compact: bool = False
+    perm: np.ndarray | None = None  # complex shifts' run order (solve_group(unpermute=False))
 
     def rotations(self):
         """The recorded rotations as (c_re, c_im, s) device tensors (ms, n),
@@ -404,15 +484,25 @@ def raise_first_failure(fail_codes, b_c, kinds):
 
 
 def solve_group(h, eigs_cplx, eigs_real, b, b_r, *, robust=True, mode="eigvec", b_c=32,
-                device=None, solver=None, compact=False):
+                device=None, solver=None, compact=False, unpermute=True):
     """Run one solve group; returns (GroupOutput, GroupSolver).
 
-    ``b``: a real n-vector used for every column (the inverse-iteration
-    start vector) or a host/device matrix (n, ncol) in the column layout.
+    ``h``: a HessenbergMatrix / array, or a DeviceHessenberg already on the
+    device.  ``b``: a real n-vector used for every column (the
+    inverse-iteration start vector) or a host/device matrix (n, ncol) in the
+    column layout.  ``unpermute=False`` leaves the complex shifts in the
+    order they ran (sorted by imaginary part) and returns that order in
+    ``GroupOutput.perm`` (None: caller order), for callers that map columns
+    themselves (the inverse-iteration drivers' output packing).
     """
-    hm = h if isinstance(h, HessenbergMatrix) else HessenbergMatrix(h)
-    _check_h(hm)
-    dh = DeviceHessenberg.of(hm, device)
+    if isinstance(h, DeviceHessenberg):
+        dh = h
+        if not dh.is_unreduced():
+            raise ConfigError("matrix must be unreduced (nonzero subdiagonal)")
+    else:
+        hm = h if isinstance(h, HessenbergMatrix) else HessenbergMatrix(h)
+        _check_h(hm)
+        dh = DeviceHessenberg.of(hm, device)
     mc = len(np.atleast_1d(eigs_cplx)) if eigs_cplx is not None else 0
     mr = len(np.atleast_1d(eigs_real)) if eigs_real is not None else 0
     gs = solver or GroupSolver(dh, b_r, mc, mr, compact=compact)
@@ -434,9 +524,12 @@ def solve_group(h, eigs_cplx, eigs_real, b, b_r, *, robust=True, mode="eigvec", 
     if perm is not None and not broadcast:  # right-hand sides follow their shifts
         bt = bt[torch.from_numpy(_col_index(perm, mc, mr)).to(bt.device)].contiguous()
     nfail = gs.launch(bt, broadcast, robust=robust, mode=mode)
-    if perm is not None:
+    if perm is not None and unpermute:
         _unpermute(gs, perm)
-    return gs.output(nfail), gs
+        perm = None
+    out = gs.output(nfail)
+    out.perm = perm
+    return out, gs
 
 
 def _col_index(perm, mc, mr):

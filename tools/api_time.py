@@ -30,7 +30,7 @@ def main():
         r = hsrq3in(h, sel, cfg)
         t1 = time.perf_counter()
         print(f"hsrq3in call {i}: {1e3 * (t1 - t0):.1f} ms, converged {int(r.converged.sum())}/{sel.size}",
-              r.extras.get("phase_ms", ""), flush=True)
+              {k: round(v, 1) for k, v in r.extras.get("host_ms", {}).items()}, flush=True)
         del r
 
 
