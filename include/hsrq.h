@@ -127,6 +127,18 @@ int64_t hsrq_solve_group(const double* H, int64_t ldh, int64_t n, int32_t b_r,
                          double* log2norm, int64_t* fail, int32_t robust, int32_t mode, void* ws,
                          size_t ws_bytes, void* stream);
 
+/* hsrq_solve_group with the caller's overflow budget: omega > 0 is
+ * OverflowBudget.omega (overflow.py:31-47; dhsrq3 / chsrq3 budget=,
+ * backsolve.py:342-346) in (0, DBL_MAX/2]; omega = 0 means the default
+ * DBL_MAX/2/b_r (robust = 0 ignores it: omega = inf). */
+int64_t hsrq_solve_group_omega(const double* H, int64_t ldh, int64_t n, int32_t b_r,
+                               const double* lam_re, const double* lam_im, int64_t m_cplx,
+                               int64_t m_real, const double* B, int64_t ldb, int32_t b_broadcast,
+                               double* X, int64_t ldx, double* c_re, double* c_im, double* s,
+                               int64_t ldc, int32_t* seg_exp, int32_t* alpha_exp, double* norms,
+                               double* log2norm, int64_t* fail, int32_t robust, int32_t mode,
+                               double omega, void* ws, size_t ws_bytes, void* stream);
+
 /* Same, but asynchronous: returns 0 once every kernel is enqueued (or a
  * negative error); the failure count is left in the workspace and read with
  * hsrq_failure_count (which synchronises the stream). */

@@ -62,6 +62,11 @@
 static int g_stop_jt = -1;
 void oracle_set_stop(int jt) { g_stop_jt = jt; }
 
+/* Test hook (oracle_set_omega): the caller's OverflowBudget.omega for the
+ * next solves (dhsrq3 / chsrq3 budget=); 0 = the default DBL_MAX/2/b_r. */
+static double g_omega = 0.0;
+void oracle_set_omega(double omega) { g_omega = omega; }
+
 static int64_t pack_status(int64_t kind, int64_t shift, int64_t row) {
     return kind * ((int64_t)1 << 42) + (shift << 21) + row;
 }
@@ -998,7 +1003,10 @@ static int64_t solve_batch(const double* H, int64_t n, int b_r, int cplx_, int b
                            int* tile) {
     const int N = (int)((n + b_r - 1) / b_r);
     const int ncol = cplx_ ? 2 * b : b;
-    const double omega = robust ? (1.7976931348623157e308 / 2.0) / (double)b_r : INFINITY;
+    /* OverflowBudget.for_grid (overflow.py:41-47), or the caller's budget
+     * (backsolve.py:342-346) set with oracle_set_omega */
+    const double omega = robust ? (g_omega > 0.0 ? g_omega : (1.7976931348623157e308 / 2.0) / (double)b_r)
+                                : INFINITY;
     int64_t* ends = (int64_t*)malloc(sizeof(int64_t) * N);
     for (int t = 0; t < N; t++) ends[t] = (int64_t)(t + 1) * b_r < n ? (int64_t)(t + 1) * b_r : n;
     double* cross = (double*)malloc(sizeof(double) * (size_t)n * N * ncol); /* (n, N, ncol) */

@@ -316,6 +316,14 @@ def householder_hessenberg(a):
     return h, q
 
 
+def set_omega(omega):
+    """Test hook: solves use OverflowBudget(omega) (0 / None: DBL_MAX/2/b_r)."""
+    L = lib()
+    L.oracle_set_omega.restype = None
+    L.oracle_set_omega.argtypes = [ctypes.c_double]
+    L.oracle_set_omega(float(omega or 0.0))
+
+
 def set_stop(jt):
     """Test hook: oracle solves end after tile column jt's updates (no
     backtransform; x holds solved tiles >= jt and updated rhs below); -1 off."""

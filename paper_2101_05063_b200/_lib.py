@@ -28,6 +28,11 @@ SIGNATURES = {
         [_p, _i64, _i64, _i32, _p, _p, _i64, _i64, _p, _i64, _i32, _p, _i64, _p, _p, _p, _i64,
          _p, _p, _p, _p, _p, _i32, _i32, _p, _sz, _p],
     ),
+    "hsrq_solve_group_omega": (
+        _i64,
+        [_p, _i64, _i64, _i32, _p, _p, _i64, _i64, _p, _i64, _i32, _p, _i64, _p, _p, _p, _i64,
+         _p, _p, _p, _p, _p, _i32, _i32, _f64, _p, _sz, _p],
+    ),
     "hsrq_solve_group_async": (
         _i64,
         [_p, _i64, _i64, _i32, _p, _p, _i64, _i64, _p, _i64, _i32, _p, _i64, _p, _p, _p, _i64,

@@ -649,7 +649,8 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
                    int32_t b_broadcast, double* X, int64_t ldx, double* c_re, double* c_im,
                    double* s, int64_t ldc, int32_t* seg_exp, int32_t* alpha_exp, double* norms,
                    double* log2norm, int64_t* fail, int32_t robust, int32_t mode, void* ws,
-                   size_t ws_bytes, cudaStream_t stream, const HostFeed* feed = nullptr) {
+                   size_t ws_bytes, cudaStream_t stream, const HostFeed* feed = nullptr,
+                   double omega_in = 0.0) {
   g_launches = 0;
   if (n < 1 || b_r < 1 || b_r > MAXK || b_r > n || mc < 0 || mr < 0 || mc + mr < 1 || ldx < n ||
       ldh < n || ldc < n) {
@@ -703,7 +704,9 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     c.diag_tl_jt = atoi(getenv("HSRQ_TIMELINE"));
     g_tl = tl;
   }
-  c.omega = robust ? (1.7976931348623157e308 / 2.0) / (double)b_r
+  // OverflowBudget.for_grid (overflow.py:41-47) unless the caller passes
+  // its own budget (dhsrq3 / chsrq3 budget=, backsolve.py:342-346)
+  c.omega = robust ? (omega_in > 0.0 ? omega_in : (1.7976931348623157e308 / 2.0) / (double)b_r)
                    : HUGE_VAL;
   // the crossover block shares X's leading dimension
   if (ldx != n) {
@@ -1172,9 +1175,25 @@ int64_t hsrq_solve_group(const double* H, int64_t ldh, int64_t n, int32_t b_r,
                          int64_t ldc, int32_t* seg_exp, int32_t* alpha_exp, double* norms,
                          double* log2norm, int64_t* fail, int32_t robust, int32_t mode, void* ws,
                          size_t ws_bytes, void* stream) {
+  return hsrq_solve_group_omega(H, ldh, n, b_r, lam_re, lam_im, m_cplx, m_real, B, ldb,
+                                b_broadcast, X, ldx, c_re, c_im, s, ldc, seg_exp, alpha_exp, norms,
+                                log2norm, fail, robust, mode, 0.0, ws, ws_bytes, stream);
+}
+
+int64_t hsrq_solve_group_omega(const double* H, int64_t ldh, int64_t n, int32_t b_r,
+                               const double* lam_re, const double* lam_im, int64_t m_cplx,
+                               int64_t m_real, const double* B, int64_t ldb, int32_t b_broadcast,
+                               double* X, int64_t ldx, double* c_re, double* c_im, double* s,
+                               int64_t ldc, int32_t* seg_exp, int32_t* alpha_exp, double* norms,
+                               double* log2norm, int64_t* fail, int32_t robust, int32_t mode,
+                               double omega, void* ws, size_t ws_bytes, void* stream) {
+  if (!(omega >= 0.0) || omega > 1.7976931348623157e308 / 2.0) {
+    snprintf(g_err, sizeof(g_err), "omega=%g outside (0, maxfloat/2]", omega);
+    return HSRQ_ERR_CONFIG;
+  }
   int64_t r = solve_impl(H, ldh, n, b_r, lam_re, lam_im, m_cplx, m_real, B, ldb, b_broadcast, X,
                          ldx, c_re, c_im, s, ldc, seg_exp, alpha_exp, norms, log2norm, fail,
-                         robust, mode, ws, ws_bytes, (cudaStream_t)stream);
+                         robust, mode, ws, ws_bytes, (cudaStream_t)stream, nullptr, omega);
   if (r < 0) return r;
   WsLayout L = ws_layout(n, b_r, m_cplx, m_real);
   unsigned long long nf = 0;

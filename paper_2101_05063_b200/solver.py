@@ -263,8 +263,10 @@ class GroupSolver:
         self.lam_re.copy_(torch.from_numpy(np.ascontiguousarray(lam.real)))
         self.lam_im.copy_(torch.from_numpy(np.ascontiguousarray(lam.imag)))
 
-    def launch(self, B, broadcast, robust=True, mode="eigvec", stream=None, sync=True):
-        """Enqueue the whole sweep.  B: device (n,) vector (broadcast) or (ncol, n)."""
+    def launch(self, B, broadcast, robust=True, mode="eigvec", stream=None, sync=True,
+               omega=None):
+        """Enqueue the whole sweep.  B: device (n,) vector (broadcast) or (ncol, n).
+        ``omega``: the caller's OverflowBudget.omega (default DBL_MAX/2/b_r)."""
         stream = stream or torch.cuda.current_stream(self.dh.device)
         mode_i = {"solve": 0, "eigvec": 1}[mode] | (MODE_COMPACT_ROTATIONS if self.compact else 0)
         args = (
@@ -275,8 +277,13 @@ class GroupSolver:
             _ptr(self.fail), int(bool(robust)), mode_i, _ptr(self.ws), self.ws_bytes,
             ctypes.c_void_p(stream.cuda_stream),
         )
-        fn = self.lib.hsrq_solve_group if sync else self.lib.hsrq_solve_group_async
-        r = fn(*args)
+        if omega is not None:
+            if not sync:
+                raise ConfigError("a custom overflow budget needs a synchronous launch")
+            r = self.lib.hsrq_solve_group_omega(*args[:24], float(omega), *args[24:])
+        else:
+            fn = self.lib.hsrq_solve_group if sync else self.lib.hsrq_solve_group_async
+            r = fn(*args)
         if r < 0:
             raise RuntimeError(f"hsrq_solve_group failed ({r}): {_lib.last_error()}")
         return int(r)
@@ -484,7 +491,7 @@ def raise_first_failure(fail_codes, b_c, kinds):
 
 
 def solve_group(h, eigs_cplx, eigs_real, b, b_r, *, robust=True, mode="eigvec", b_c=32,
-                device=None, solver=None, compact=False, unpermute=True):
+                device=None, solver=None, compact=False, unpermute=True, omega=None):
     """Run one solve group; returns (GroupOutput, GroupSolver).
 
     ``h``: a HessenbergMatrix / array, or a DeviceHessenberg already on the
@@ -523,7 +530,7 @@ def solve_group(h, eigs_cplx, eigs_real, b, b_r, *, robust=True, mode="eigvec", 
     bt = bt.to(dh.device)
     if perm is not None and not broadcast:  # right-hand sides follow their shifts
         bt = bt[torch.from_numpy(_col_index(perm, mc, mr)).to(bt.device)].contiguous()
-    nfail = gs.launch(bt, broadcast, robust=robust, mode=mode)
+    nfail = gs.launch(bt, broadcast, robust=robust, mode=mode, omega=omega)
     if perm is not None and unpermute:
         _unpermute(gs, perm)
         perm = None

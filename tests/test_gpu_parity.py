@@ -290,3 +290,31 @@ def test_tile_backtransform_bitwise(dev):
         assert np.array_equal(x.cpu().numpy().T, g[f"{t}_xout"]), t
         assert np.array_equal(norms.cpu().numpy(), g[f"{t}_norms"]), t
         assert np.array_equal(np.ldexp(1.0, aexp.cpu().numpy()), g[f"{t}_alpha"]), t
+
+
+def test_budget_solves_match_reference(dev):
+    """dhsrq3 / chsrq3 with budget=OverflowBudget(omega) (backsolve.py:342-346)
+    vs the reference's outputs (golden budget.npz, omega 1 / 8 / 1e3 / 2^600:
+    the guards fire at ordinary magnitudes, well-conditioned systems):
+    exponents exact, x to 1e-12 (the GEMM's summation order is the only
+    non-bitwise step; the oracle matches the reference bit for bit,
+    test_oracle_golden.py::test_budget_solves)."""
+    from types import SimpleNamespace
+
+    from paper_2101_05063_b200 import chsrq3, dhsrq3
+
+    g = golden("budget")
+    fired = 0
+    for tag in g["tags"]:
+        b_r, b_c, mode, cplx = (int(v) for v in g[f"{tag}_cfg"])
+        f = chsrq3 if cplx else dhsrq3
+        r = f(g[f"{tag}_h"], g[f"{tag}_lam"], g[f"{tag}_b"], b_r=b_r, b_c=b_c,
+              mode=("solve", "eigvec")[mode], budget=SimpleNamespace(omega=float(g[f"{tag}_omega"])))
+        assert np.array_equal(r.segment_scales.alpha, g[f"{tag}_seg"]), tag
+        assert np.array_equal(r.alpha, g[f"{tag}_alpha"]), tag
+        fired += int(np.any(g[f"{tag}_seg"] < 1.0))
+        xr = g[f"{tag}_x"]
+        for l in range(xr.shape[1]):
+            sc = np.max(np.abs(xr[:, l]))
+            assert np.max(np.abs(r.x[:, l] - xr[:, l])) <= 1e-12 * sc, (tag, l)
+    assert fired >= 12

@@ -163,3 +163,24 @@ def test_householder_hessenberg_oracle(oracle):
     t = tags[9]  # random_unreduced: already Hessenberg
     h, q = oracle.householder_hessenberg(g[f"{t}_a"])
     assert np.array_equal(h, g[f"{t}_a"]) and np.array_equal(q, np.eye(h.shape[0]))
+
+
+def test_budget_solves(oracle, same_blas):
+    """dhsrq3/chsrq3 with a caller's OverflowBudget (backsolve.py:342-346,
+    golden budget.npz: omega 1 / 8 / 1e3 / 2^600): bitwise like the default budget."""
+    g = golden("budget")
+    try:
+        for tag in g["tags"]:
+            b_r, b_c, mode, cplx = (int(v) for v in g[f"{tag}_cfg"])
+            oracle.set_omega(float(g[f"{tag}_omega"]))
+            r = oracle.solve(g[f"{tag}_h"], g[f"{tag}_lam"], g[f"{tag}_b"], b_r, b_c,
+                             mode=("solve", "eigvec")[mode])
+            assert np.array_equal(r.segment_scales, g[f"{tag}_seg"]), tag
+            assert np.array_equal(r.alpha, g[f"{tag}_alpha"]), tag
+            xr = g[f"{tag}_x"]
+            if same_blas:
+                assert np.array_equal(r.x, xr), tag
+            else:
+                assert np.max(np.abs(r.x - xr)) <= 1e-12 * (np.max(np.abs(xr)) or 1.0), tag
+    finally:
+        oracle.set_omega(0.0)

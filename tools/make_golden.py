@@ -180,6 +180,44 @@ def gen_solves():
     save("solves", tags=np.array(tags), **store)
 
 
+def gen_budget():
+    """dhsrq3 / chsrq3 with a caller's OverflowBudget (backsolve.py:342-346):
+    small omegas make every guard fire at ordinary magnitudes."""
+    from hessrq.overflow import OverflowBudget
+
+    store = {}
+    tags = []
+    rng = np.random.default_rng(11)
+    for n, b_r, seed in ((48, 16, 1), (70, 32, 2), (65, 64, 3)):
+        h = random_unreduced(n, seed)
+        nrm = h.infinity_norm()
+        lam = nrm * rng.uniform(-1, 1, 3)  # well-conditioned systems: the guards fire
+        clam = nrm * (rng.uniform(-1, 1, 3) + 1j * rng.uniform(0.05, 1, 3))  # because omega is small
+        b = rng.standard_normal((n, lam.size))
+        cb = rng.standard_normal((n, clam.size)) + 1j * rng.standard_normal((n, clam.size))
+        for omega in (1.0, 8.0, 1e3, 2.0 ** 600):
+            for mode in ("solve", "eigvec"):
+                for cplx, L, B in ((False, lam, b), (True, clam, cb)):
+                    if L.size == 0:
+                        continue
+                    f = chsrq3 if cplx else dhsrq3
+                    r = f(h, L, B, b_r=b_r, b_c=2, robust=True, mode=mode,
+                          budget=OverflowBudget(omega=omega))
+                    t = f"b{len(tags)}"
+                    store[f"{t}_h"] = np.asfortranarray(h.data)
+                    store[f"{t}_lam"] = L
+                    store[f"{t}_b"] = B
+                    store[f"{t}_cfg"] = np.array([b_r, 2, {"solve": 0, "eigvec": 1}[mode],
+                                                  int(cplx)], dtype=np.int64)
+                    store[f"{t}_omega"] = np.array(omega)
+                    store[f"{t}_x"] = r.x
+                    store[f"{t}_alpha"] = r.alpha
+                    store[f"{t}_seg"] = r.segment_scales.alpha
+                    store[f"{t}_norms"] = r.norms if r.norms is not None else np.full(L.size, np.nan)
+                    tags.append(t)
+    save("budget", tags=np.array(tags), **store)
+
+
 def gen_inviter():
     store = {}
     # H1 with known eigenvalues, real and complex parts
