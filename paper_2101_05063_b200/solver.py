@@ -383,7 +383,25 @@ class HostGroupSolver:
         ticket for ``wait_ticket``; the host buffers must stay alive until then."""
         h = np.asarray(h)
         if not (h.flags.f_contiguous and h.dtype == np.float64):
+            if not wait:  # a converted copy could be freed while the copy engine reads it
+                raise ConfigError("asynchronous launch needs a float64 Fortran-ordered h")
             h = np.asfortranarray(h, dtype=np.float64)
+        # the C ABI reads raw pointers: wrong dtypes / strides would be read silently
+        for name, a, dt in (("lam_re", lam_re, np.float64), ("lam_im", lam_im, np.float64),
+                            ("b", b, np.float64), ("out.X", out.X, np.float64),
+                            ("out.seg_exp", out.seg_exp, np.int32),
+                            ("out.alpha_exp", out.alpha_exp, np.int32),
+                            ("out.norms", out.norms, np.float64),
+                            ("out.log2norm", out.log2norm, np.float64),
+                            ("out.fail", out.fail, np.int64)):
+            if a is None and name == "lam_im":
+                continue
+            if not (isinstance(a, np.ndarray) and a.dtype == dt and a.flags.c_contiguous):
+                raise ConfigError(f"{name} must be a C-contiguous {np.dtype(dt).name} array")
+        if lam_re.size != self.ms or (lam_im is not None and lam_im.size != self.ms):
+            raise ConfigError("shift arrays must hold m_cplx + m_real entries")
+        if b.size != (self.n if broadcast else self.n * self.ncol) or out.X.size != self.n * self.ncol:
+            raise ConfigError("right-hand side / output sizes do not match the solver's shape")
         stream = stream or torch.cuda.current_stream(self.device)
         P = lambda a: ctypes.c_void_p(a.ctypes.data) if a is not None else ctypes.c_void_p(0)
         mode_i = {"solve": 0, "eigvec": 1}[mode]
