@@ -221,6 +221,10 @@ int64_t hsrq_host_wait(int64_t ticket);
 
 /* Guard-path event counters (diagnostics): out_host[16]; reset != 0 zeroes them. */
 int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset);
+/* Diagnostics build -DHSRQ_STEPPROF only (returns 0 otherwise): per-phase
+ * clock64 sums of the complex diagonal sweep's steps ([0..9]) and the number
+ * of profiled warps ([15]); out_host holds 16 entries. */
+int64_t hsrq_debug_stepprof(int64_t* out_host, int32_t reset);
 
 /* Kernel launches issued by the last solve on this thread (for accounting). */
 int64_t hsrq_last_launch_count(void);
@@ -243,6 +247,12 @@ void hsrq_phase_times(double* out_host);
  * 0 = off, -1 = automatic.  Every variant computes identical results;
  * unknown combinations fall back to the default kernel.  Returns 0. */
 int32_t hsrq_tune_diag(int32_t dp, int32_t dwr, int32_t dwc, int32_t wsr, int32_t wsc);
+/* Rotation-ahead warp pairs (k_diag_cplx_rx: the rotation chain one step
+ * ahead of the solution chain) for the complex sweep at 16 / 32 lanes per
+ * shift: np = 4 / 8 pairs per CTA, 0 = off, -1 = automatic (16-lane pairs,
+ * 8 per CTA, where the automatic choice is 32 lanes per shift).  Results
+ * are bit-identical either way. */
+int32_t hsrq_tune_diag_rx(int32_t np);
 
 /*
  * Tile-level entry points (parity tests against the reference kernels).

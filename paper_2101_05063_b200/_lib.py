@@ -61,6 +61,7 @@ SIGNATURES = {
     "hsrq_last_launch_count": (_i64, []),
     "hsrq_set_timing": (None, [_i32]),
     "hsrq_tune_diag": (_i32, [_i32, _i32, _i32, _i32, _i32]),
+    "hsrq_tune_diag_rx": (_i32, [_i32]),
     "hsrq_phase_times": (None, [_p]),
     "hsrq_tile_diag": (
         _i64,
@@ -72,6 +73,7 @@ SIGNATURES = {
     "hsrq_protect_update_pair_batch": (_i64, [_p, _p, _p, _p, _p, _f64, _i64, _p, _p, _p]),
     "hsrq_hypot_batch": (_i64, [_p, _p, _i64, _p, _p]),
     "hsrq_debug_counters": (_i64, [_p, _i32]),
+    "hsrq_debug_stepprof": (_i64, [_p, _i32]),
     "hsrq_compact_encode": (_i64, [_i64, _i32, _p, _p, _p, _p, _p, _p]),
     "hsrq_compact_decode": (_i64, [_i64, _i32, _p, _p, _p, _p, _p, _p]),
     "hsrq_hessenberg_workspace_bytes": (_sz, [_i64]),

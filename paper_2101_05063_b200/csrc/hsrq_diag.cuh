@@ -24,6 +24,24 @@
 constexpr double DSLACK = 1.0 + 0x1p-46;
 constexpr unsigned FULL = 0xffffffffu;
 
+// Per-step phase profile (diagnostics build -DHSRQ_STEPPROF, read with
+// hsrq_debug_stepprof): clock64 marks inside the one-warp complex sweep's
+// step, summed over the steps of warp 0 of every CTA.
+#ifdef HSRQ_STEPPROF
+__device__ unsigned long long g_stepprof[16];
+#define SP_DECL long long sp_t0 = 0, sp_acc[12] = {0}; int sp_i = 0;
+#define SP_START() (sp_t0 = clock64(), sp_i = 0)
+#define SP_MARK() { const long long t_ = clock64(); sp_acc[sp_i++] += t_ - sp_t0; sp_t0 = t_; }
+#define SP_FLUSH(n) if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) == 0) { \
+    for (int i_ = 0; i_ < (n); i_++) atomicAdd(&g_stepprof[i_], (unsigned long long)sp_acc[i_]); \
+    atomicAdd(&g_stepprof[15], 1ULL); }
+#else
+#define SP_DECL
+#define SP_START() ((void)0)
+#define SP_MARK() ((void)0)
+#define SP_FLUSH(n) ((void)0)
+#endif
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   int sz = valid ? 8 : 0;
@@ -578,14 +596,18 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
   }
   HSRQ_SYNCWARP();
   int gexp = 0;
+  SP_DECL
   for (int kp = k - 1; kp >= 1; --kp) {
+    SP_START();
     const double* hcol = hb + cur * MAXK;  // column kp-1, rows 0..kp
     if (kp >= 2) fill_col(c, a, hb + (cur ^ 1) * MAXK, kp - 2, kp, lane);
     const cplx vk = mk(Vr[IX(kp)], Vi[IX(kp)]);
     cplx xk = mk(Xr[IX(kp)], Xi[IX(kp)]);
     const double av = hcol[kp];
+    SP_MARK();  // 0: column prefetch issue, row kp reads
     const double absv = ghypot(vk.re, vk.im);
     const double r = ghypot(av, absv);
+    SP_MARK();  // 1: two glibc hypots
     if (live && r == 0.0) {
       if (pl == 0) record_fail(c, a, q, HSRQ_KIND_DEGENERATE, kp);
       live = false;
@@ -598,6 +620,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
       if (pl == 0) record_fail(c, a, q, HSRQ_KIND_SINGULAR, kp);
       live = false;
     }
+    SP_MARK();  // 2: three divisions, pivot, rotation store
     xb = gmax<DP>(xb);
     vb = gmax<DP>(vb);
     if (robust && live) {  // guard 1 (robust_trsv_complex :501-508)
@@ -620,7 +643,9 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
         }
       }
     }
+    SP_MARK();  // 3: group maxima, guard 1
     xk = cdiv(xk, d);
+    SP_MARK();  // 4: complex pivot division
     // guard 2 (:510-523): protect_update(max|x_i|, max|r_i|, |x_kp|), i < kp
     bool exact2 = false;
     double rb = 0.0;
@@ -630,6 +655,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
       if (pl == 0) HSRQ_COUNT(7);
       if (pl == 0 && exact2) HSRQ_COUNT(4);
     }
+    SP_MARK();  // 5: guard-2 bound test
 #ifdef HSRQ_EXP_NOEXACT2
     exact2 = false;  // timing experiment only: results are wrong
 #endif
@@ -705,6 +731,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
         gexp += e;
       }
     }
+    SP_MARK();  // 6: guard-2 certification / exact maxima / rescale
     if (pl == (kp % DP)) {
       Xr[IX(kp)] = xk.re;
       Xi[IX(kp)] = xk.im;
@@ -726,6 +753,7 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
       Xr[IX(i)] = x.re;
       Xi[IX(i)] = x.im;
     }
+    SP_MARK();  // 7: row update
     if (pl == (kp - 1) % DP) {  // the shifted row (diagonal entry h - lambda)
       const int i = kp - 1;
       const double hi = hcol[i];
@@ -742,10 +770,13 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
     }
     xb = nxb;
     vb = nvb;
+    SP_MARK();  // 8: shifted row
     cp_wait<0>();
     HSRQ_SYNCWARP();
+    SP_MARK();  // 9: column prefetch wait, warp barrier
     cur ^= 1;
   }
+  SP_FLUSH(10);
   // j = 0: cross-tile rotation (creduce_diag :449-463) and R[0,0] (:546-550)
   const cplx v0 = mk(Vr[IX(0)], Vi[IX(0)]);
   cplx x0 = mk(Xr[IX(0)], Xi[IX(0)]);

@@ -254,6 +254,7 @@ __global__ void k_zero_bop(double* Bop, int64_t count) {
 
 #include "hsrq_diag.cuh"
 #include "hsrq_diag_ws.cuh"
+#include "hsrq_diag_rx.cuh"
 
 #include "hsrq_panel.cuh"
 
@@ -398,6 +399,8 @@ struct DiagVariant {
 DiagVariant g_force_r = {0, 0}, g_force_c = {0, 0};
 int g_diag_ws = -1;    // complex sweep warp pairs per CTA (k_diag_cplx_ws); 0 = off
 int g_diag_ws_r = -1;  // real sweep warp pairs per CTA (k_diag_real_ws); 0 = off
+int g_diag_rx = -1;    // rotation-ahead complex sweep (k_diag_cplx_rx): pairs per CTA, 0 = off,
+                       // -1 = automatic (DP-16 pairs, 8 per CTA, where one warp per shift is picked)
 
 template <int DP, int NP>
 size_t diag_ws_smem() {
@@ -408,6 +411,7 @@ size_t diag_ws_smem_r() {
   return sizeof(double) * (MAXK + NP * (2 * MAXK * (32 / DP) + 3 * MAXK + 16 * (32 / DP)));
 }
 #define HSRQ_DIAG_WS(X) X(4, 1) X(4, 2) X(4, 3) X(8, 2) X(8, 3) X(8, 4) X(16, 2) X(16, 4) X(32, 4) X(32, 8)
+#define HSRQ_DIAG_RX(X) X(16, 4) X(16, 8) X(32, 4) X(32, 8)
 #define HSRQ_DIAG_WSR(X) X(4, 2) X(4, 3) X(4, 4) X(8, 2) X(8, 4) X(16, 2) X(16, 4) X(32, 4) X(32, 8)
 
 template <int DP, int DW, bool CPLX>
@@ -480,6 +484,14 @@ bool diag_attrs() {
                 "attr diag wsr");
   HSRQ_DIAG_WSR(HSRQ_ATTR_WR)
 #undef HSRQ_ATTR_WR
+#define HSRQ_ATTR_RX(DP, NP)                                                               \
+  ok = ok && ck(cudaFuncSetAttribute(k_diag_cplx_rx<DP, NP>,                               \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                                     (int)diag_rx_smem<DP, NP>()),                         \
+                "attr diag rx");
+  HSRQ_DIAG_RX(HSRQ_ATTR_RX)
+#undef HSRQ_ATTR_RX
+  if (const char* w = getenv("HSRQ_DIAG_RX")) g_diag_rx = atoi(w);
 #undef HSRQ_ATTR_R
 #undef HSRQ_ATTR_C
 #undef HSRQ_ATTR_W
@@ -538,8 +550,34 @@ void diag_launch_ws(const Ctx& c, const DiagArgs& a, cudaStream_t s) {
                            s>>>(c, a);
 }
 
+template <int DP, int NP>
+void diag_launch_rx(const Ctx& c, const DiagArgs& a, cudaStream_t s) {
+  const int per = NP * (32 / DP);
+  k_diag_cplx_rx<DP, NP><<<(unsigned)((a.count + per - 1) / per), NP * 64, diag_rx_smem<DP, NP>(),
+                           s>>>(c, a);
+}
+
 void diag_launch(bool cplx, const Ctx& c, const DiagArgs& a, cudaStream_t s) {
   const DiagVariant v = diag_pick(cplx, a.count);
+  // Rotation-ahead pairs (k_diag_cplx_rx).  Automatic where the pick is one
+  // warp per shift (the 1/8 shards of config 5): pairs at 16 lanes per shift,
+  // 8 per CTA -- the same 16 shifts per SM as the one-warp sweep, the
+  // rotation chain beside the solution chain (1/8 shard: 96.7 -> 89.8 ms).
+  if (cplx && !a.tile_mode) {
+    if (g_diag_rx < 0 && v.dp == 32 && g_force_c.dp == 0) {
+      diag_launch_rx<16, 8>(c, a, s);
+      return;
+    }
+#define HSRQ_LAUNCH_RX(DP, NP)        \
+  if (v.dp == DP && g_diag_rx == NP) { \
+    diag_launch_rx<DP, NP>(c, a, s);  \
+    return;                           \
+  }
+    if (g_diag_rx > 0) {
+      HSRQ_DIAG_RX(HSRQ_LAUNCH_RX)
+    }
+#undef HSRQ_LAUNCH_RX
+  }
   // warp-specialised complex sweep: automatic at DP 4 (all of config 5 on
   // one GPU: 506 -> 495 ms); measured no gain at DP >= 8 (the lookahead
   // shards), where the sweep runs beside the panel
@@ -1373,6 +1411,23 @@ int64_t hsrq_debug_timeline(unsigned long long* out_host) {
              : HSRQ_ERR_CUDA;
 }
 
+int64_t hsrq_debug_stepprof(int64_t* out_host, int32_t reset) {
+#ifdef HSRQ_STEPPROF
+  unsigned long long v[16];
+  if (cudaMemcpyFromSymbol(v, g_stepprof, sizeof(v)) != cudaSuccess) return HSRQ_ERR_CUDA;
+  for (int i = 0; i < 16; i++) out_host[i] = (int64_t)v[i];
+  if (reset) {
+    unsigned long long z[16] = {0};
+    if (cudaMemcpyToSymbol(g_stepprof, z, sizeof(z)) != cudaSuccess) return HSRQ_ERR_CUDA;
+  }
+  return 16;
+#else
+  (void)out_host;
+  (void)reset;
+  return 0;
+#endif
+}
+
 int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset) {
   unsigned long long v[16];
   if (cudaMemcpyFromSymbol(v, g_ctr, sizeof(v)) != cudaSuccess) return HSRQ_ERR_CUDA;
@@ -1393,6 +1448,11 @@ int32_t hsrq_tune_diag(int32_t dp, int32_t dwr, int32_t dwc, int32_t wsr, int32_
   g_diag_ws_r = wsr;
   g_diag_ws = wsc;
   return 0;
+}
+int32_t hsrq_tune_diag_rx(int32_t np) {
+  diag_attrs();  // reads the environment once; the explicit setting wins
+  g_diag_rx = (np == 4 || np == 8) ? np : (np < 0 ? -1 : 0);
+  return g_diag_rx;
 }
 void hsrq_phase_times(double* out_host) {
   for (int i = 0; i < 5; i++) g_phase_ms[i] = 0.0;

@@ -33,6 +33,8 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 # (DP, real DW, complex DW, real warp pairs, complex warp pairs): the one-GPU
 # config-5 choice first, then the shard choices (diag_pick), then the other
 # compiled warp-pair shapes
+# (the 6th entry, where present: rotation-ahead pairs per CTA, hsrq_tune_diag_rx;
+# 0 = off; -1 = automatic, which at a forced 32 lanes per shift stays off)
 DIAG_VARIANTS = [
     (4, 4, 2, 0, 2),    # config 5, one GPU (automatic)
     (4, 4, 2, 0, 0),    # one-warp complex sweep at DP 4
@@ -41,8 +43,11 @@ DIAG_VARIANTS = [
     (8, 6, 4, 2, 2),
     (16, 16, 16, 0, 0),  # 1/4 shard
     (16, 16, 16, 2, 2),
-    (32, 16, 16, 0, 0),  # 1/8 shard
+    (32, 16, 16, 0, 0),  # one warp per shift
     (32, 16, 16, 4, 4),
+    (16, 16, 16, 0, 0, 8),  # 1/8 shard (automatic): 16-lane rotation-ahead pairs
+    (16, 16, 16, 0, 0, 4),
+    (32, 16, 16, 0, 0, 8),
 ]
 BT_GS = [4, 8, 16, 32]
 
@@ -68,6 +73,7 @@ def lib(dev, monkeypatch):
     L = _lib.load()
     yield L
     L.hsrq_tune_diag(0, 0, 0, -1, -1)  # back to the automatic choice
+    L.hsrq_tune_diag_rx(-1)
     monkeypatch.delenv("HSRQ_BT_G", raising=False)
 
 
@@ -138,7 +144,8 @@ def test_diag_variants_match_oracle_and_each_other(dev, lib, oracle, n, b_r, see
     dh = DeviceHessenberg(HessenbergMatrix(h), dev)
     base = None
     for v in DIAG_VARIANTS:
-        lib.hsrq_tune_diag(*v)
+        lib.hsrq_tune_diag(*v[:5])
+        lib.hsrq_tune_diag_rx(v[5] if len(v) > 5 else 0)
         gs = GroupSolver(dh, b_r, ec.size, er.size)
         gs.set_shifts(ec, er)
         assert gs.launch(B, True) == 0
@@ -164,6 +171,7 @@ def test_backtransform_lanes_match_oracle_and_each_other(dev, lib, oracle, monke
     B = torch.from_numpy(start).to(dev)
     dh = DeviceHessenberg(HessenbergMatrix(h), dev)
     lib.hsrq_tune_diag(*DIAG_VARIANTS[0])
+    lib.hsrq_tune_diag_rx(0)
     base = None
     for g in BT_GS:
         monkeypatch.setenv("HSRQ_BT_G", str(g))
@@ -194,7 +202,8 @@ def test_variants_solve_mode_explicit_rhs(dev, lib):
     for v in DIAG_VARIANTS:
         for g in (8, 32):
             os.environ["HSRQ_BT_G"] = str(g)
-            lib.hsrq_tune_diag(*v)
+            lib.hsrq_tune_diag(*v[:5])
+            lib.hsrq_tune_diag_rx(v[5] if len(v) > 5 else 0)
             gs = GroupSolver(dh, 128, ec.size, er.size)
             gs.set_shifts(ec, er)
             assert gs.launch(B, False, mode="solve") == 0
@@ -229,12 +238,15 @@ def test_production_selection_at_scale_is_variant_invariant(dev, lib):
     B = torch.full((n,), rho, dtype=torch.float64, device=dev)
     dh = DeviceHessenberg(HessenbergMatrix(h), dev)
     outs = []
-    for v, g in ((None, None), ((32, 16, 16, 0, 0), "32"), ((8, 6, 4, 0, 0), "16")):
+    for v, g in ((None, None), ((32, 16, 16, 0, 0), "32"), ((8, 6, 4, 0, 0), "16"),
+                 ((16, 16, 16, 0, 0, 8), "32")):
         if v is None:
             lib.hsrq_tune_diag(0, 0, 0, -1, -1)
+            lib.hsrq_tune_diag_rx(-1)
             os.environ.pop("HSRQ_BT_G", None)
         else:
-            lib.hsrq_tune_diag(*v)
+            lib.hsrq_tune_diag(*v[:5])
+            lib.hsrq_tune_diag_rx(v[5] if len(v) > 5 else 0)
             os.environ["HSRQ_BT_G"] = g
         gs = GroupSolver(dh, 128, ec.size, er.size)
         gs.set_shifts(ec, er)
@@ -244,3 +256,4 @@ def test_production_selection_at_scale_is_variant_invariant(dev, lib):
     os.environ.pop("HSRQ_BT_G", None)
     _same(outs[0], outs[1], "auto vs DP32/G32")
     _same(outs[0], outs[2], "auto vs DP8/G16")
+    _same(outs[0], outs[3], "auto vs rotation-ahead DP16 pairs/G32")

@@ -31,7 +31,8 @@ from paper_2101_05063_b200.core import HessenbergMatrix  # noqa: E402
 from paper_2101_05063_b200.solver import DeviceHessenberg, GroupSolver  # noqa: E402
 
 VARIANTS = [(4, 4, 2, 0, 2), (4, 4, 2, 0, 0), (4, 4, 2, 2, 2), (8, 6, 4, 0, 0), (8, 6, 4, 2, 2),
-            (16, 16, 16, 0, 0), (16, 16, 16, 2, 2), (32, 16, 16, 0, 0), (32, 16, 16, 4, 4)]
+            (16, 16, 16, 0, 0), (16, 16, 16, 2, 2), (32, 16, 16, 0, 0), (32, 16, 16, 4, 4),
+            (16, 16, 16, 0, 0, 8), (32, 16, 16, 0, 0, 4)]  # 6th: rotation-ahead pairs
 CASES = [(300, 64, 3, 8, 16), (515, 100, 6, 8, 40)]  # n, b_r, seed, real, complex
 
 
@@ -48,7 +49,8 @@ def run_all():
         B = torch.full((n,), 1e300, dtype=torch.float64, device=dev)
         for vi, v in enumerate(VARIANTS):
             for la in ("0", "1"):
-                L.hsrq_tune_diag(*v)
+                L.hsrq_tune_diag(*v[:5])
+                L.hsrq_tune_diag_rx(v[5] if len(v) > 5 else 0)
                 os.environ["HSRQ_BT_G"] = str((4, 8, 16, 32)[vi % 4])
                 os.environ["HSRQ_LOOKAHEAD"] = la
                 gs = GroupSolver(dh, b_r, ec.size, er.size)
@@ -67,6 +69,7 @@ def run_all():
     for k in ("HSRQ_BT_G", "HSRQ_LOOKAHEAD"):
         os.environ.pop(k, None)
     L.hsrq_tune_diag(0, 0, 0, -1, -1)
+    L.hsrq_tune_diag_rx(-1)
     torch.cuda.synchronize()
     return res
 
