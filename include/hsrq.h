@@ -377,6 +377,35 @@ int64_t hsrq_pack_download(const double* X, int64_t ldx, int64_t n, int64_t m,
                            const int64_t* re_col, const int64_t* im_col, const double* im_sign,
                            int32_t cplx_out, void* out_host, void* stream);
 
+/*
+ * hsrq_tile_update: one off-diagonal tile through the sweep's own panel
+ * kernels (the diagonal sweep's operand code, k_scalars, k_panel) -- the
+ * reference operator API update_rupdate / cupdate_crupdate
+ * (numba_backend.py:198-311, 579-736) and reduce_offdiag / creduce_offdiag
+ * (:109-125, 467-490) on one tile, for tile-level parity.  Device pointers,
+ * row-major like the reference's tiles; b shifts, real or complex
+ * (cplx = 1: interleaved re/im columns, 2b wide).
+ *   htile      m x k: H[is:ie, js-1:je-1] (column 0 = the column left of tile jt)
+ *   rright     m x b / m x 2b: crossover column jt on the tile's rows
+ *   alpha_exp  b: log2 alpha (the scale of x_below)
+ *   xbelow     k x b / k x 2b: the solved tile jt
+ *   lam_re, lam_im   b shifts (lam_im / c_im NULL when real)
+ *   shift_active     1: super-diagonal tile (lambda on the last row, for the
+ *              update and the crossover); 0: a far tile (no lambda)
+ *   c_re, c_im, s    k x b rotations of tile jt
+ *   beta_exp   in: log2 beta (scale of b); out: log2 delta
+ *   b_io       in/out m x b / m x 2b right-hand side tile
+ *   rleft      out (or NULL): the new crossover column jt-1 on the tile's rows
+ *   omega      0: DBL_MAX/2/m (OverflowBudget.for_tile_rows(m))
+ * Requires 2 <= k <= m <= 128.  Stream-ordered; returns 0 or HSRQ_ERR_*.
+ */
+int64_t hsrq_tile_update(int32_t m, int32_t k, int32_t b, int32_t cplx, const double* htile,
+                         const double* rright, const int32_t* alpha_exp, const double* xbelow,
+                         const double* lam_re, const double* lam_im, int32_t shift_active,
+                         const double* c_re, const double* c_im, const double* s,
+                         int32_t* beta_exp, double* b_io, double* rleft, int32_t robust,
+                         double omega, void* stream);
+
 /* Elementwise device evaluations for bit-level parity of the scalar helpers. */
 int64_t hsrq_protect_update_batch(const double* bnorm, const double* hnorm, const double* xnorm,
                                   double omega, int64_t count, double* out, void* stream);

@@ -67,6 +67,9 @@ SIGNATURES = {
         _i64,
         [_i32, _i32, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _f64, _p],
     ),
+    "hsrq_tile_update": (
+        _i64, [_i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _p, _p, _p, _p, _i32,
+               _f64, _p]),
     "hsrq_tile_backtransform": (
         _i64, [_i64, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _i32, _f64, _p]),
     "hsrq_protect_update_batch": (_i64, [_p, _p, _p, _f64, _i64, _p, _p]),

@@ -177,6 +177,12 @@ __device__ __forceinline__ void put_rot(const Ctx& c, const DiagArgs& a, int64_t
   }
 }
 
+template <int DP>
+__device__ __forceinline__ void diag_real_operands(const Ctx& c, const DiagArgs& a, int64_t q,
+                                                   int64_t col, bool live, int pl, int grp, int k,
+                                                   double* V, double* Xs, double c0, double s0,
+                                                   double x0);
+
 // The last step of a real shift's sweep -- cross-tile rotation
 // (reduce_diag :94-105) and the last pivot (:178-192) -- the write-back of
 // x and the panel operands (update_rupdate :246-253); shared by k_diag_real
@@ -241,7 +247,25 @@ __device__ __forceinline__ void diag_real_tail(const Ctx& c, const DiagArgs& a, 
   }
   if (live && pl == 0) c.E[(int64_t)a.jt * c.ms + q] += gexp;
   if (a.jt == 0) return;
+  diag_real_operands<DP>(c, a, q, col, live, pl, grp, k, V, Xs, c0, s0, x0);
+#undef VV
+#undef XX
+}
 
+// Panel operands of a real shift after its sweep (update_rupdate :246-253,
+// reduce_offdiag :109-125 as a linear map): W_j = c_j prod_{t<j} s_t, P, the
+// rotated solution Z and the step scalars -- from the tile's recorded
+// rotations (c_re / s at rot_off) and its final x in shared memory.  Shared
+// by k_diag_real, the chain warp of k_diag_real_ws and the tile-level update
+// entry (k_tile_operands).
+template <int DP>
+__device__ __forceinline__ void diag_real_operands(const Ctx& c, const DiagArgs& a, int64_t q,
+                                                   int64_t col, bool live, int pl, int grp, int k,
+                                                   double* V, double* Xs, double c0, double s0,
+                                                   double x0) {
+  constexpr int DG = 32 / DP;
+#define VV(i) V[(i) * DG + grp]
+#define XX(i) Xs[(i) * DG + grp]
   // ---- panel operands: W_j = c_j prod_{t<j} s_t, P; Z (update_rupdate :246-253) ----
   double* bw = c.Bop + (2 * col) * KP;
   double* bz = c.Bop + (2 * col + 1) * KP;

@@ -682,6 +682,33 @@ struct HostFeed {
                          // and 1 for the async one (the next solve hides the download)
 };
 
+// Raised dynamic shared-memory limits of the panel and diagonal kernels,
+// once per device (diag_attrs does the diagonal ones).
+int64_t ensure_attrs() {
+  static bool attr_done[MAX_DEVICES] = {};
+  const size_t panel_smem = sizeof(PanelSmem);
+  const int cur_dev = current_device();
+  if (cur_dev < 0 || cur_dev >= MAX_DEVICES) return HSRQ_ERR_CONFIG;
+  if (!diag_attrs()) return HSRQ_ERR_CUDA;
+  std::unique_lock<std::mutex> setup_lock(g_setup_mu);
+  if (!attr_done[cur_dev]) {
+    if (
+        !ck(cudaFuncSetAttribute(k_panel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)panel_smem), "attr panel") ||
+        !ck(cudaFuncSetAttribute(k_panel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)panel_smem), "attr panel") ||
+        !ck(cudaFuncSetAttribute(k_panel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)panel_smem), "attr panel") ||
+        !ck(cudaFuncSetAttribute(k_panel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)panel_smem), "attr panel") ||
+        !ck(cudaFuncSetAttribute(k_panel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)panel_smem), "attr panel fast"))
+      return HSRQ_ERR_CUDA;
+    attr_done[cur_dev] = true;
+  }
+  return 0;
+}
+
 int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const double* lam_re,
                    const double* lam_im, int64_t mc, int64_t mr, const double* B, int64_t ldb,
                    int32_t b_broadcast, double* X, int64_t ldx, double* c_re, double* c_im,
@@ -752,28 +779,8 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     return HSRQ_ERR_CONFIG;
   }
 
-  static bool attr_done[MAX_DEVICES] = {};
   const size_t panel_smem = sizeof(PanelSmem);
-  const int cur_dev = current_device();
-  if (cur_dev < 0 || cur_dev >= MAX_DEVICES) return HSRQ_ERR_CONFIG;
-  if (!diag_attrs()) return HSRQ_ERR_CUDA;
-  std::unique_lock<std::mutex> setup_lock(g_setup_mu);
-  if (!attr_done[cur_dev]) {
-    if (
-        !ck(cudaFuncSetAttribute(k_panel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)panel_smem), "attr panel") ||
-        !ck(cudaFuncSetAttribute(k_panel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)panel_smem), "attr panel") ||
-        !ck(cudaFuncSetAttribute(k_panel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)panel_smem), "attr panel") ||
-        !ck(cudaFuncSetAttribute(k_panel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)panel_smem), "attr panel") ||
-        !ck(cudaFuncSetAttribute(k_panel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)panel_smem), "attr panel fast"))
-      return HSRQ_ERR_CUDA;
-    attr_done[cur_dev] = true;
-  }
-  setup_lock.unlock();
+  if (const int64_t r = ensure_attrs(); r != 0) return r;
   // Optional per-launch timing: events around every launch, one sync at the end.
   const int nev = 6 * c.N + 6;
   cudaEvent_t* ev = nullptr;
@@ -1640,3 +1647,4 @@ int64_t hsrq_compact_decode(int64_t count, int32_t cplx, const double* t1, const
 }  // extern "C"
 
 #include "hsrq_hostio.cuh"
+#include "hsrq_tile_update.cuh"

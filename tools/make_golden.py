@@ -218,6 +218,64 @@ def gen_budget():
     save("budget", tags=np.array(tags), **store)
 
 
+def gen_update_tiles():
+    """update_rupdate / cupdate_crupdate and reduce_offdiag / creduce_offdiag
+    on single tiles (numba_backend.py:109-125, 198-311, 467-490, 579-736):
+    tile shapes of full, short (ragged last tile) and odd heights, shifted
+    and far tiles, robust and plain, magnitudes where every guard fires."""
+    store = {}
+    tags = []
+    rng = np.random.default_rng(21)
+    for m, k in ((128, 128), (128, 77), (64, 64), (37, 21)):
+        for cplx in (False, True):
+            for shifted in (True, False):
+                for robust, scale in ((True, 1.0), (True, 1e300), (False, 1.0)):
+                    b = 5
+                    ht = rng.standard_normal((m, k))
+                    th = rng.uniform(0, 2 * np.pi, (k, b))
+                    if cplx:
+                        ph = rng.uniform(0, 2 * np.pi, (k, b))
+                        cre, cim, s = np.cos(th) * np.cos(ph), np.cos(th) * np.sin(ph), np.sin(th)
+                        lre, lim = rng.standard_normal(b), rng.uniform(0.1, 2, b)
+                        rr = rng.standard_normal((m, 2 * b))
+                        xb = scale * rng.standard_normal((k, 2 * b))
+                        bio = scale * rng.standard_normal((m, 2 * b))
+                    else:
+                        cre, cim, s = np.cos(th), None, np.sin(th)
+                        lre, lim = rng.standard_normal(b), None
+                        rr = rng.standard_normal((m, b))
+                        xb = scale * rng.standard_normal((k, b))
+                        bio = scale * rng.standard_normal((m, b))
+                    aexp = rng.integers(-6, 1, b).astype(np.int32)
+                    bexp = rng.integers(-6, 1, b).astype(np.int32)
+                    alpha, beta = np.ldexp(1.0, aexp), np.ldexp(1.0, bexp)
+                    omega = _DMAX / 2.0 / m if robust else math.inf
+                    lz = lre if shifted else np.zeros(b)
+                    lzi = (lim if shifted else np.zeros(b)) if cplx else None
+                    bo = bio.copy()
+                    bt = beta.copy()
+                    rl = np.empty_like(rr)
+                    if cplx:
+                        K.cupdate_crupdate(ht, rr, alpha, xb, lz, lzi, shifted, cre, cim, s, bt, bo,
+                                           robust, omega)
+                        K.creduce_offdiag(ht, lz, lzi, cre, cim, s, rr, rl)
+                    else:
+                        K.update_rupdate(ht, rr, alpha, xb, lz, shifted, cre, s, bt, bo, robust,
+                                         omega)
+                        K.reduce_offdiag(ht, lz, cre, s, rr, rl)
+                    t = f"u{len(tags)}"
+                    store.update({f"{t}_cfg": np.array([m, k, b, int(cplx), int(shifted),
+                                                        int(robust)], dtype=np.int64),
+                                  f"{t}_ht": ht, f"{t}_rr": rr, f"{t}_aexp": aexp, f"{t}_xb": xb,
+                                  f"{t}_lre": lre, f"{t}_cre": cre, f"{t}_s": s, f"{t}_bexp": bexp,
+                                  f"{t}_bio": bio, f"{t}_out_b": bo, f"{t}_out_beta": bt,
+                                  f"{t}_out_rleft": rl})
+                    if cplx:
+                        store.update({f"{t}_lim": lim, f"{t}_cim": cim})
+                    tags.append(t)
+    save("update_tiles", tags=np.array(tags), **store)
+
+
 def gen_inviter():
     store = {}
     # H1 with known eigenvalues, real and complex parts
