@@ -52,7 +52,7 @@ def build(force=False, verbose=False, variant=None, defines=()):
         return LIB
     extra = [f"-D{d}" for d in defines]
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp",
-           *SOURCES, "-lcublas"]
+           *SOURCES]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

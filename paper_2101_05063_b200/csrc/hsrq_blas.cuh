@@ -1,0 +1,334 @@
+// hsrq_blas.cuh -- the fp64 dense kernels of the front end (included by
+// hsrq_hessenberg.cu): the DGEMM / DGEMV / DTRMM / DTRMV / DSCAL shapes the
+// blocked Householder reduction and the back-multiplication need, written
+// for sm_100a instead of calling cuBLAS.
+//
+//   k_dgemm<TA, TB>  C = alpha op(A) op(B) + beta C (column-major): 128 x 64
+//                    CTA tiles, K chunks of 16 staged through shared memory
+//                    with a register prefetch of the next chunk, eight warps
+//                    of 32 x 32 on fp64 tensor cores (mma.sync m16n8k4 f64 =
+//                    DMMA.8x8x4; FP64 has no tcgen05 kind on sm_100a).
+//   k_gemv_n         y = alpha A x + beta y: the reduction's level-2 product
+//                    A[:, j+1:] v streams the trailing matrix once per column
+//                    (HBM-bound, its inherent cost): 256-row x 128-column
+//                    blocks, two rows per thread as 16-byte loads, eight
+//                    columns in flight, partial sums per column chunk reduced
+//                    in a fixed order (deterministic); few columns: a thread
+//                    per row.
+//   k_gemv_t         y = alpha A^T x + beta y: a CTA per column.
+//   k_trmm_ru        W = W T (T upper, at most 64 x 64, in shared memory).
+//   k_trmv_u         x = op(T) x for the panel's small triangular factor.
+
+namespace hblas {
+
+constexpr int GM = 128, GN = 64, GK = 16;
+
+__device__ __forceinline__ void mma_f64(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// op(A)[i][k] and op(B)[k][j] with zero fill outside the matrix
+template <bool T>
+__device__ __forceinline__ double opa(const double* A, int64_t lda, int M, int K, int i, int k) {
+  if (i >= M || k >= K) return 0.0;
+  return T ? A[k + (int64_t)i * lda] : A[i + (int64_t)k * lda];
+}
+template <bool T>
+__device__ __forceinline__ double opb(const double* B, int64_t ldb, int K, int N, int k, int j) {
+  if (k >= K || j >= N) return 0.0;
+  return T ? B[j + (int64_t)k * ldb] : B[k + (int64_t)j * ldb];
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, double alpha, const double* A,
+                                               int64_t lda, const double* B, int64_t ldb,
+                                               double beta, double* C, int64_t ldc) {
+  __shared__ double As[GK][GM + 4];  // [k][m]
+  __shared__ double Bs[GN][GK + 4];  // [n][k]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m0 = blockIdx.x * GM, n0 = blockIdx.y * GN;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int g = lane >> 2, t4 = lane & 3;
+  double ra[8], rb[4];
+  // thread -> element maps, coalesced along the contiguous index of each operand
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int idx = tid + e * 256;
+      int i, k;
+      if (TA) {
+        i = idx / GK;
+        k = idx % GK;
+      } else {
+        k = idx / GM;
+        i = idx % GM;
+      }
+      ra[e] = opa<TA>(A, lda, M, K, m0 + i, k0 + k);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int idx = tid + e * 256;
+      int k, j;
+      if (TB) {
+        k = idx / GN;
+        j = idx % GN;
+      } else {
+        j = idx / GK;
+        k = idx % GK;
+      }
+      rb[e] = opb<TB>(B, ldb, K, N, k0 + k, n0 + j);
+    }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int idx = tid + e * 256;
+      int i, k;
+      if (TA) {
+        i = idx / GK;
+        k = idx % GK;
+      } else {
+        k = idx / GM;
+        i = idx % GM;
+      }
+      As[k][i] = ra[e];
+    }
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int idx = tid + e * 256;
+      int k, j;
+      if (TB) {
+        k = idx / GN;
+        j = idx % GN;
+      } else {
+        j = idx / GK;
+        k = idx % GK;
+      }
+      Bs[j][k] = rb[e];
+    }
+  };
+  double acc[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
+  load(0);
+  for (int k0 = 0; k0 < K; k0 += GK) {
+    __syncthreads();
+    store();
+    __syncthreads();
+    if (k0 + GK < K) load(k0 + GK);  // next chunk in flight during the MMAs
+#pragma unroll
+    for (int kk = 0; kk < GK; kk += 4) {
+      double af[2][2], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++) {
+        const int r = wm * 32 + mi * 16 + g;
+        af[mi][0] = As[kk + t4][r];
+        af[mi][1] = As[kk + t4][r + 8];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ni++) bf[ni] = Bs[wn * 32 + ni * 8 + g][kk + t4];
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 4; ni++) mma_f64(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+    }
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+    for (int ni = 0; ni < 4; ni++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int r = m0 + wm * 32 + mi * 16 + g + (e >= 2 ? 8 : 0);
+        const int cc = n0 + wn * 32 + ni * 8 + 2 * t4 + (e & 1);
+        if (r < M && cc < N) {
+          double* p = C + r + (int64_t)cc * ldc;
+          const double v = alpha * acc[mi][ni][e];
+          *p = beta == 0.0 ? v : v + beta * *p;
+        }
+      }
+}
+
+// y = alpha A x + beta y, A column-major m x n: partial sums of column chunks
+// of 128 into part[chunk][row], then k_gemv_n_reduce in chunk order.
+constexpr int GV_THREADS = 128, GV_ROWS = 2 * GV_THREADS, GV_COLS = 128;
+// two rows per thread (16-byte loads when the rows are 16-byte aligned), eight
+// column loads in flight per thread
+__global__ void __launch_bounds__(GV_THREADS) k_gemv_n_part(int m, int n, const double* A,
+                                                            int64_t lda, const double* x,
+                                                            int64_t incx, double* part) {
+  const int r = blockIdx.x * GV_ROWS + 2 * threadIdx.x;
+  const int c0 = blockIdx.y * GV_COLS, c1 = min(n, c0 + GV_COLS);
+  __shared__ double xs[GV_COLS];
+  for (int j = threadIdx.x; j < c1 - c0; j += GV_THREADS) xs[j] = x[(int64_t)(c0 + j) * incx];
+  __syncthreads();
+  if (r >= m) return;
+  const double* a = A + r + (int64_t)c0 * lda;
+  const int nc = c1 - c0;
+  double s0[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};
+  const bool vec = r + 1 < m && ((reinterpret_cast<uintptr_t>(a) | (lda * 8)) & 15) == 0;
+  int j = 0;
+  if (vec) {
+    for (; j + 8 <= nc; j += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) v[u] = *reinterpret_cast<const double2*>(a + (int64_t)(j + u) * lda);
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        s0[u & 3] += v[u].x * xs[j + u];
+        s1[u & 3] += v[u].y * xs[j + u];
+      }
+    }
+    for (; j < nc; j++) {
+      const double2 v = *reinterpret_cast<const double2*>(a + (int64_t)j * lda);
+      s0[0] += v.x * xs[j];
+      s1[0] += v.y * xs[j];
+    }
+  } else {
+    for (; j < nc; j++) {
+      s0[j & 3] += a[(int64_t)j * lda] * xs[j];
+      if (r + 1 < m) s1[j & 3] += a[(int64_t)j * lda + 1] * xs[j];
+    }
+  }
+  part[(int64_t)blockIdx.y * m + r] = (s0[0] + s0[1]) + (s0[2] + s0[3]);
+  if (r + 1 < m) part[(int64_t)blockIdx.y * m + r + 1] = (s1[0] + s1[1]) + (s1[2] + s1[3]);
+}
+__global__ void k_gemv_n_reduce(int m, int nchunk, const double* part, double alpha, double beta,
+                                double* y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  double s = 0.0;
+#pragma unroll 8
+  for (int c = 0; c < nchunk; c++) s += part[(int64_t)c * m + r];
+  y[r] = beta == 0.0 ? alpha * s : alpha * s + beta * y[r];
+}
+
+// y = alpha A x + beta y for few columns (n <= 64): one thread per row.
+__global__ void k_gemv_n_small(int m, int n, const double* A, int64_t lda, const double* x,
+                               int64_t incx, double alpha, double beta, double* y) {
+  __shared__ double xs[64];
+  if (threadIdx.x < n) xs[threadIdx.x] = x[(int64_t)threadIdx.x * incx];
+  __syncthreads();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  double s0 = 0.0, s1 = 0.0;
+  int j = 0;
+  for (; j + 2 <= n; j += 2) {
+    s0 += A[r + (int64_t)j * lda] * xs[j];
+    s1 += A[r + (int64_t)(j + 1) * lda] * xs[j + 1];
+  }
+  if (j < n) s0 += A[r + (int64_t)j * lda] * xs[j];
+  const double s = s0 + s1;
+  y[r] = beta == 0.0 ? alpha * s : alpha * s + beta * y[r];
+}
+
+// y = alpha A^T x + beta y, A column-major m x n: one CTA per column.
+__global__ void __launch_bounds__(256) k_gemv_t(int m, int n, const double* A, int64_t lda,
+                                                const double* x, double alpha, double beta,
+                                                double* y) {
+  __shared__ double red[8];
+  const int col = blockIdx.x;
+  const double* a = A + (int64_t)col * lda;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < m; i += 256) s += a[i] * x[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; w++) t += red[w];
+    y[col] = beta == 0.0 ? alpha * t : alpha * t + beta * y[col];
+  }
+}
+
+// W = W T in place, W rows x p column-major (ldw), T p x p upper (ldt),
+// p <= 64: one thread per row, T in shared memory.
+__global__ void k_trmm_ru(int rows, int p, const double* T, int64_t ldt, double* W, int64_t ldw) {
+  __shared__ double ts[64][65];
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int i = e % p, j = e / p;
+    ts[i][j] = i <= j ? T[i + (int64_t)j * ldt] : 0.0;
+  }
+  __syncthreads();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double w[64];
+#pragma unroll 8
+  for (int i = 0; i < 64; i++) w[i] = i < p ? W[r + (int64_t)i * ldw] : 0.0;
+  for (int j = p - 1; j >= 0; j--) {  // column j uses w[0..j]
+    double s = 0.0;
+    for (int i = 0; i <= j; i++) s += w[i] * ts[i][j];
+    W[r + (int64_t)j * ldw] = s;
+  }
+}
+
+// x = T x (trans = 0) or T^T x (trans = 1), T p x p upper (ldt), one block.
+__global__ void k_trmv_u(int p, const double* T, int64_t ldt, double* x, int trans) {
+  __shared__ double xs[64];
+  const int i = threadIdx.x;
+  if (i < p) xs[i] = x[i];
+  __syncthreads();
+  if (i < p) {
+    double s = 0.0;
+    if (!trans) {
+      for (int j = i; j < p; j++) s += T[i + (int64_t)j * ldt] * xs[j];
+    } else {
+      for (int j = 0; j <= i; j++) s += T[j + (int64_t)i * ldt] * xs[j];
+    }
+    x[i] = s;
+  }
+}
+
+// x *= *alpha (a device scalar)
+__global__ void k_dscal(int n, const double* alpha, double* x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] *= *alpha;
+}
+
+// ---- host wrappers (stream-ordered, column-major, cuBLAS argument order) ----
+
+inline void dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
+                  int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                  cudaStream_t s) {
+  if (M <= 0 || N <= 0) return;
+  const dim3 grid((unsigned)((M + GM - 1) / GM), (unsigned)((N + GN - 1) / GN));
+  if (!ta && !tb)
+    k_dgemm<false, false><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (!ta && tb)
+    k_dgemm<false, true><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (ta && !tb)
+    k_dgemm<true, false><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else
+    k_dgemm<true, true><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+// y = alpha op(A) x + beta y; part: scratch of ceil(n / 128) * m doubles (no-trans only)
+inline void dgemv(bool trans, int m, int n, double alpha, const double* A, int64_t lda,
+                  const double* x, int64_t incx, double beta, double* y, double* part,
+                  cudaStream_t s) {
+  if (!trans) {
+    if (m <= 0) return;
+    if (n <= 64) {  // the panel's few-column products (also n = 0: y = beta y)
+      k_gemv_n_small<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, n, A, lda, x, incx, alpha,
+                                                                 beta, y);
+      return;
+    }
+    const int nchunk = (n + GV_COLS - 1) / GV_COLS;
+    k_gemv_n_part<<<dim3((unsigned)((m + GV_ROWS - 1) / GV_ROWS), (unsigned)nchunk), GV_THREADS, 0,
+                    s>>>(m, n, A, lda, x, incx, part);
+    k_gemv_n_reduce<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(m, nchunk, part, alpha, beta, y);
+  } else {
+    if (n <= 0) return;
+    k_gemv_t<<<(unsigned)n, 256, 0, s>>>(m, n, A, lda, x, alpha, beta, y);
+  }
+}
+
+}  // namespace hblas

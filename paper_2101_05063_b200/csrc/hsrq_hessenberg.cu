@@ -12,18 +12,21 @@
 // accumulated as Q_p = I - V T V^T with Y = A V T, so only the panel needs
 // the level-2 product A[:, j+1:] v per column (HBM-bound GEMV, the inherent
 // cost of the reduction); the trailing two-sided update and the Q update are
-// fp64 GEMMs (cuBLAS DGEMM, DMMA on sm_100a: plain library GEMMs).  The
-// per-column vector work -- the reflector with the reference's skip rule and
-// sign convention, the T column -- runs in one small kernel per column.
-#include <cublas_v2.h>
+// fp64 GEMMs on the tensor cores.  Every dense kernel is this library's own
+// (hsrq_blas.cuh: DMMA GEMM, streaming GEMV, the small triangular products);
+// nothing links cuBLAS.  The per-column vector work -- the reflector with the
+// reference's skip rule and sign convention, the T column -- runs in one
+// small kernel per column.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
 
 #include "../../include/hsrq.h"
 #include "hsrq_device.cuh"
+#include "hsrq_blas.cuh"
 
 namespace {
 
@@ -119,37 +122,12 @@ __global__ void k_set_identity(double* Q, int64_t n, int64_t ldq) {
   Q[c * ldq + r] = r == c ? 1.0 : 0.0;
 }
 
-struct Blas {
-  cublasHandle_t h = nullptr;
-  int dev = -1;
-};
-thread_local Blas g_blas;
-
-bool blas_ok(cublasStatus_t s, const char* what) {
-  if (s != CUBLAS_STATUS_SUCCESS) {
-    snprintf(g_herr, sizeof(g_herr), "%s: cublas status %d", what, (int)s);
-    return false;
-  }
-  return true;
-}
 bool cu_ok(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
     snprintf(g_herr, sizeof(g_herr), "%s: %s", what, cudaGetErrorString(e));
     return false;
   }
   return true;
-}
-
-cublasHandle_t handle(cudaStream_t s) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (g_blas.h == nullptr || g_blas.dev != dev) {
-    if (cublasCreate(&g_blas.h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-    g_blas.dev = dev;
-  }
-  cublasSetStream(g_blas.h, s);
-  cublasSetPointerMode(g_blas.h, CUBLAS_POINTER_MODE_HOST);
-  return g_blas.h;
 }
 
 }  // namespace
@@ -160,7 +138,9 @@ const char* hsrq_hessenberg_last_error(void) { return g_herr; }
 
 size_t hsrq_hessenberg_workspace_bytes(int64_t n) {
   const size_t nb = HB_NB;
-  return sizeof(double) * ((size_t)n * nb * 2 + nb * nb + 4 * nb + nb * (size_t)n + 256);
+  const size_t nchunk = ((size_t)n + hblas::GV_COLS - 1) / hblas::GV_COLS;
+  return sizeof(double) * ((size_t)n * nb * 2 + nb * nb + 4 * nb + nb * (size_t)n + 256 +
+                           nchunk * (size_t)n);
 }
 
 int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, int64_t n,
@@ -168,11 +148,6 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
   if (n < 1 || lda < n || (Q && ldq < n)) return HSRQ_ERR_CONFIG;
   if (ws_bytes < hsrq_hessenberg_workspace_bytes(n)) return HSRQ_ERR_WORKSPACE;
   cudaStream_t stream = (cudaStream_t)stream_;
-  cublasHandle_t h = handle(stream);
-  if (!h) {
-    snprintf(g_herr, sizeof(g_herr), "cublasCreate failed");
-    return HSRQ_ERR_CUDA;
-  }
   const int nb = HB_NB;
   double* V = (double*)ws;              // n x nb
   double* Y = V + (size_t)n * nb;       // n x nb
@@ -180,12 +155,13 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
   double* tau = T + (size_t)nb * nb;    // nb
   double* ntau = tau + nb;              // nb
   double* u = ntau + nb;                // nb
-  double* W = u + nb;                   // nb x n (also n x nb for the Q update)
-  const double one = 1.0, mone = -1.0, zero = 0.0;
+  double* W = u + nb;                   // n x nb (W^T of the left update; Q V T)
+  double* part = W + (size_t)nb * n + 256;  // GEMV partial sums
   if (Q) {
     k_set_identity<<<(unsigned)((n * n + 255) / 256), 256, 0, stream>>>(Q, n, ldq);
     if (!cu_ok(cudaGetLastError(), "identity")) return HSRQ_ERR_CUDA;
   }
+  using namespace hblas;
   for (int64_t j0 = 0; j0 < n - 2; j0 += nb) {
     const int pb = (int)std::min<int64_t>(nb, n - 2 - j0);
     const int64_t L = n - j0 - 1;  // rows j0+1 .. n-1 (support of the panel's V)
@@ -196,17 +172,11 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
       double* aj = A + j * lda;
       if (i > 0) {
         // right update of column j: a_j -= Y[:, :i] V[j, :i]^T
-        if (!blas_ok(cublasDgemv(h, CUBLAS_OP_N, (int)n, i, &mone, Y, (int)n, V + j, (int)n, &one,
-                                 aj, 1), "gemv right"))
-          return HSRQ_ERR_CUDA;
+        dgemv(false, (int)n, i, -1.0, Y, n, V + j, n, 1.0, aj, part, stream);
         // left update of rows j0+1.. : a -= V T^T V^T a
-        if (!blas_ok(cublasDgemv(h, CUBLAS_OP_T, (int)L, i, &one, V + j0 + 1, (int)n, aj + j0 + 1,
-                                 1, &zero, u, 1), "gemv vta") ||
-            !blas_ok(cublasDtrmv(h, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, i,
-                                 T, nb, u, 1), "trmv") ||
-            !blas_ok(cublasDgemv(h, CUBLAS_OP_N, (int)L, i, &mone, V + j0 + 1, (int)n, u, 1, &one,
-                                 aj + j0 + 1, 1), "gemv left"))
-          return HSRQ_ERR_CUDA;
+        dgemv(true, (int)L, i, 1.0, V + j0 + 1, n, aj + j0 + 1, 1, 0.0, u, part, stream);
+        k_trmv_u<<<1, 64, 0, stream>>>(i, T, nb, u, 1);
+        dgemv(false, (int)L, i, -1.0, V + j0 + 1, n, u, 1, 1.0, aj + j0 + 1, part, stream);
       }
       double* vi = V + (size_t)i * n;
       k_reflector<<<1, HB_THREADS, 0, stream>>>(aj, n, j, vi, tau + i, ntau + i,
@@ -214,56 +184,38 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
       if (!cu_ok(cudaGetLastError(), "reflector")) return HSRQ_ERR_CUDA;
       // Y[:, i] = tau (A[:, j+1:] v - Y[:, :i] (V^T v)); T[:i, i] = -tau T[:i, :i] (V^T v)
       double* yi = Y + (size_t)i * n;
-      if (!blas_ok(cublasDgemv(h, CUBLAS_OP_N, (int)n, (int)(n - j - 1), &one, A + (j + 1) * lda,
-                               (int)lda, vi + j + 1, 1, &zero, yi, 1), "gemv Av"))
-        return HSRQ_ERR_CUDA;
+      dgemv(false, (int)n, (int)(n - j - 1), 1.0, A + (j + 1) * lda, lda, vi + j + 1, 1, 0.0, yi,
+            part, stream);
       if (i > 0) {
         double* ti = T + (size_t)i * nb;
-        if (!blas_ok(cublasDgemv(h, CUBLAS_OP_T, (int)L, i, &one, V + j0 + 1, (int)n, vi + j0 + 1,
-                                 1, &zero, ti, 1), "gemv vtv") ||
-            !blas_ok(cublasDgemv(h, CUBLAS_OP_N, (int)n, i, &mone, Y, (int)n, ti, 1, &one, yi, 1),
-                     "gemv y") ||
-            !blas_ok(cublasDtrmv(h, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, i,
-                                 T, nb, ti, 1), "trmv t"))
-          return HSRQ_ERR_CUDA;
-        cublasSetPointerMode(h, CUBLAS_POINTER_MODE_DEVICE);
-        const bool ok = blas_ok(cublasDscal(h, i, ntau + i, ti, 1), "scal t");
-        cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST);
-        if (!ok) return HSRQ_ERR_CUDA;
+        dgemv(true, (int)L, i, 1.0, V + j0 + 1, n, vi + j0 + 1, 1, 0.0, ti, part, stream);
+        dgemv(false, (int)n, i, -1.0, Y, n, ti, 1, 1.0, yi, part, stream);
+        k_trmv_u<<<1, 64, 0, stream>>>(i, T, nb, ti, 0);
+        k_dscal<<<1, 64, 0, stream>>>(i, ntau + i, ti);
       }
-      cublasSetPointerMode(h, CUBLAS_POINTER_MODE_DEVICE);
-      const bool ok = blas_ok(cublasDscal(h, (int)n, tau + i, yi, 1), "scal y");
-      cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST);
-      if (!ok) return HSRQ_ERR_CUDA;
+      k_dscal<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>((int)n, tau + i, yi);
     }
     const int64_t c0 = j0 + pb, nc = n - c0;  // trailing columns
     if (nc > 0) {
       // right: A[:, c0:] -= Y V[c0:, :]^T
-      if (!blas_ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)nc, pb, &mone, Y, (int)n,
-                               V + c0, (int)n, &one, A + c0 * lda, (int)lda), "gemm right"))
-        return HSRQ_ERR_CUDA;
-      // left: A[j0+1:, c0:] -= V T^T (V^T A[j0+1:, c0:])
-      if (!blas_ok(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, pb, (int)nc, (int)L, &one, V + j0 + 1,
-                               (int)n, A + c0 * lda + j0 + 1, (int)lda, &zero, W, pb), "gemm vta") ||
-          !blas_ok(cublasDtrmm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
-                               CUBLAS_DIAG_NON_UNIT, pb, (int)nc, &one, T, nb, W, pb, W, pb),
-                   "trmm") ||
-          !blas_ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)L, (int)nc, pb, &mone, V + j0 + 1,
-                               (int)n, W, pb, &one, A + c0 * lda + j0 + 1, (int)lda), "gemm left"))
-        return HSRQ_ERR_CUDA;
+      dgemm(false, true, (int)n, (int)nc, pb, -1.0, Y, n, V + c0, n, 1.0, A + c0 * lda, lda,
+            stream);
+      // left: A[j0+1:, c0:] -= V T^T (V^T A[j0+1:, c0:]), with W^T = A^T V (nc x pb)
+      dgemm(true, false, (int)nc, pb, (int)L, 1.0, A + c0 * lda + j0 + 1, lda, V + j0 + 1, n, 0.0,
+            W, nc, stream);
+      k_trmm_ru<<<(unsigned)((nc + 127) / 128), 128, 0, stream>>>((int)nc, pb, T, nb, W, nc);
+      dgemm(false, true, (int)L, (int)nc, pb, -1.0, V + j0 + 1, n, W, nc, 1.0,
+            A + c0 * lda + j0 + 1, lda, stream);
     }
     if (Q) {
       // Q[:, j0+1:] -= (Q[:, j0+1:] V T) V^T
-      if (!blas_ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, pb, (int)L, &one,
-                               Q + (j0 + 1) * ldq, (int)ldq, V + j0 + 1, (int)n, &zero, W, (int)n),
-                   "gemm qv") ||
-          !blas_ok(cublasDtrmm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
-                               CUBLAS_DIAG_NON_UNIT, (int)n, pb, &one, T, nb, W, (int)n, W, (int)n),
-                   "trmm q") ||
-          !blas_ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)L, pb, &mone, W, (int)n,
-                               V + j0 + 1, (int)n, &one, Q + (j0 + 1) * ldq, (int)ldq), "gemm q"))
-        return HSRQ_ERR_CUDA;
+      dgemm(false, false, (int)n, pb, (int)L, 1.0, Q + (j0 + 1) * ldq, ldq, V + j0 + 1, n, 0.0, W,
+            n, stream);
+      k_trmm_ru<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>((int)n, pb, T, nb, W, n);
+      dgemm(false, true, (int)n, (int)L, pb, -1.0, W, n, V + j0 + 1, n, 1.0, Q + (j0 + 1) * ldq,
+            ldq, stream);
     }
+    if (!cu_ok(cudaGetLastError(), "panel kernels")) return HSRQ_ERR_CUDA;
   }
   if (!cu_ok(cudaStreamSynchronize(stream), "sync")) return HSRQ_ERR_CUDA;
   return 0;
@@ -273,13 +225,9 @@ int64_t hsrq_backmultiply(const double* Q, int64_t ldq, int64_t n, const double*
                           int64_t ncol, double* Z, int64_t ldz, void* stream_) {
   if (n < 1 || ncol < 0 || ldq < n || ldx < n || ldz < n) return HSRQ_ERR_CONFIG;
   if (ncol == 0) return 0;
-  cublasHandle_t h = handle((cudaStream_t)stream_);
-  if (!h) return HSRQ_ERR_CUDA;
-  const double one = 1.0, zero = 0.0;
-  if (!blas_ok(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, (int)ncol, (int)n, &one, Q,
-                           (int)ldq, X, (int)ldx, &zero, Z, (int)ldz), "gemm qx"))
-    return HSRQ_ERR_CUDA;
-  return 0;
+  hblas::dgemm(false, false, (int)n, (int)ncol, (int)n, 1.0, Q, ldq, X, ldx, 0.0, Z, ldz,
+               (cudaStream_t)stream_);
+  return cu_ok(cudaGetLastError(), "gemm qx") ? 0 : HSRQ_ERR_CUDA;
 }
 
 }  // extern "C"
