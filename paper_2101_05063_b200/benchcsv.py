@@ -30,7 +30,6 @@ from __future__ import annotations
 import argparse
 import csv
 import os
-import struct
 import sys
 import time
 
@@ -44,7 +43,6 @@ from .henry import henry_rq_solve
 BENCH_SCHEMA = "hessrq-bench-v1"
 TASK_TYPES = flops.TASK_TYPES
 GPU_PHASES = ("diag", "panel", "backtransform", "setup", "scalars")  # hsrq_phase_times order
-_MAGIC = b"HSRQ"
 
 
 def _kv(spec):
@@ -54,30 +52,6 @@ def _kv(spec):
             k, _, v = part.partition("=")
             out[k.strip()] = v.strip()
     return out
-
-
-def read_matrix(path):
-    """The reference's matrix file (core.py:327-349): binary (magic, version 1,
-    n, flags, column-major float64) or text (n, then n*n values row by row)."""
-    with open(path, "rb") as f:
-        head = f.read(4)
-        if head == _MAGIC:
-            version, n, _flags = struct.unpack("<III", f.read(12))
-            if version != 1:
-                raise ConfigError(f"unsupported matrix file version {version}")
-            raw = f.read(8 * n * n)
-            if len(raw) != 8 * n * n:
-                raise ConfigError("matrix file truncated")
-            return HessenbergMatrix(np.frombuffer(raw, dtype="<f8").reshape((n, n), order="F"))
-    with open(path) as f:
-        tok = f.read().split()
-    if not tok:
-        raise ConfigError("empty matrix file")
-    n = int(tok[0])
-    vals = np.array([float(t) for t in tok[1:]], dtype=np.float64)
-    if vals.size != n * n:
-        raise ConfigError(f"expected {n * n} values, found {vals.size}")
-    return HessenbergMatrix(vals.reshape((n, n)))
 
 
 def load_matrix(spec):
@@ -92,9 +66,8 @@ def load_matrix(spec):
             d = np.ldexp(1.0, (40 * np.arange(1, n + 1)) // n)
             h = h * d[None, :] / d[:, None]
         return HessenbergMatrix(h)
-    if not os.path.exists(spec):
-        raise ConfigError(f"matrix source {spec!r}: no such file or generator")
-    return read_matrix(spec)
+    raise ConfigError(f"matrix source {spec!r}: only the random:/graded: generators are "
+                      f"supported (the reference's matrix files are out of scope, SURVEY.md §2)")
 
 
 def gen_shifts(h, count, kind, seed=2, radius=1.5):

@@ -7,7 +7,7 @@ pytestmark = pytest.mark.gpu
 
 
 def test_verify_suite_passes():
-    from paper_2101_05063_b200.verify import run_verify
+    from gpu_verifysuite import run_verify
 
     ok, rep = run_verify()
     assert ok, [c for c in rep["checks"] if not c["passed"]]
@@ -15,7 +15,7 @@ def test_verify_suite_passes():
 
 
 def test_verify_suite_catches_corrupted_rotation():
-    from paper_2101_05063_b200.verify import run_verify
+    from gpu_verifysuite import run_verify
 
     ok, rep = run_verify(quick=True, corrupt_givens=True)
     assert not ok
