@@ -83,6 +83,7 @@ SIGNATURES = {
     "hsrq_hessenberg_reduce": (_i64, [_p, _i64, _p, _i64, _i64, _p, _sz, _p]),
     "hsrq_backmultiply": (_i64, [_p, _i64, _i64, _p, _i64, _i64, _p, _i64, _p]),
     "hsrq_hessenberg_last_error": (ctypes.c_char_p, []),
+    "hsrq_dgemm": (_i64, [_i32, _i32, _i64, _i64, _i64, _f64, _p, _i64, _p, _i64, _f64, _p, _i64, _p]),
     "hsrq_henry_workspace_bytes": (_sz, [_i64, _i64, _i32]),
     "hsrq_henry_solve": (_i64, [_p, _i64, _i64, _p, _i64, _i32, _p, _i64, _p, _p, _sz, _p]),
     "hsrq_h_upload": (_i64, [_p, _i32, _i64, _p, _i64, _p, _p]),

@@ -43,14 +43,21 @@ __device__ __forceinline__ double opb(const double* B, int64_t ldb, int K, int N
   return T ? B[j + (int64_t)k * ldb] : B[k + (int64_t)j * ldb];
 }
 
+// C (or, split over K, the partial block blockIdx.z of `part`) = alpha op(A)
+// op(B) + beta C over the K range [kz0, kz1).  beta != 0: the accumulators
+// start at (beta / alpha) C, loaded before the main loop, so the epilogue is
+// stores only (a read-modify-write per element after the loop would expose
+// one load latency per element).
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, double alpha, const double* A,
+__global__ void __launch_bounds__(256, 2) k_dgemm(int M, int N, int K, double alpha, const double* A,
                                                int64_t lda, const double* B, int64_t ldb,
-                                               double beta, double* C, int64_t ldc) {
+                                               double beta, double* C, int64_t ldc, int kchunk,
+                                               double* part) {
   __shared__ double As[GK][GM + 4];  // [k][m]
   __shared__ double Bs[GN][GK + 4];  // [n][k]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m0 = blockIdx.x * GM, n0 = blockIdx.y * GN;
+  const int kz0 = blockIdx.z * kchunk, kz1 = min(K, kz0 + kchunk);
   const int wm = warp & 3, wn = warp >> 2;
   const int g = lane >> 2, t4 = lane & 3;
   double ra[8], rb[4];
@@ -67,7 +74,7 @@ __global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, double alpha
         k = idx / GM;
         i = idx % GM;
       }
-      ra[e] = opa<TA>(A, lda, M, K, m0 + i, k0 + k);
+      ra[e] = opa<TA>(A, lda, M, kz1, m0 + i, k0 + k);
     }
 #pragma unroll
     for (int e = 0; e < 4; e++) {
@@ -80,7 +87,7 @@ __global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, double alpha
         j = idx / GK;
         k = idx % GK;
       }
-      rb[e] = opb<TB>(B, ldb, K, N, k0 + k, n0 + j);
+      rb[e] = opb<TB>(B, ldb, kz1, N, k0 + k, n0 + j);
     }
   };
   auto store = [&]() {
@@ -112,18 +119,24 @@ __global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, double alpha
     }
   };
   double acc[2][4][4];
+  const bool pre = part == nullptr && beta != 0.0;
+  const double ba = pre ? beta / alpha : 0.0;
 #pragma unroll
-  for (int i = 0; i < 2; i++)
+  for (int mi = 0; mi < 2; mi++)
 #pragma unroll
-    for (int j = 0; j < 4; j++)
+    for (int ni = 0; ni < 4; ni++)
 #pragma unroll
-      for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
-  load(0);
-  for (int k0 = 0; k0 < K; k0 += GK) {
+      for (int e = 0; e < 4; e++) {
+        const int r = m0 + wm * 32 + mi * 16 + g + (e >= 2 ? 8 : 0);
+        const int cc = n0 + wn * 32 + ni * 8 + 2 * t4 + (e & 1);
+        acc[mi][ni][e] = (pre && r < M && cc < N) ? ba * C[r + (int64_t)cc * ldc] : 0.0;
+      }
+  load(kz0);
+  for (int k0 = kz0; k0 < kz1; k0 += GK) {
     __syncthreads();
     store();
     __syncthreads();
-    if (k0 + GK < K) load(k0 + GK);  // next chunk in flight during the MMAs
+    if (k0 + GK < kz1) load(k0 + GK);  // next chunk in flight during the MMAs
 #pragma unroll
     for (int kk = 0; kk < GK; kk += 4) {
       double af[2][2], bf[4];
@@ -150,9 +163,10 @@ __global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, double alpha
         const int r = m0 + wm * 32 + mi * 16 + g + (e >= 2 ? 8 : 0);
         const int cc = n0 + wn * 32 + ni * 8 + 2 * t4 + (e & 1);
         if (r < M && cc < N) {
-          double* p = C + r + (int64_t)cc * ldc;
-          const double v = alpha * acc[mi][ni][e];
-          *p = beta == 0.0 ? v : v + beta * *p;
+          if (part)
+            part[((int64_t)blockIdx.z * N + cc) * M + r] = acc[mi][ni][e];
+          else
+            C[r + (int64_t)cc * ldc] = alpha * acc[mi][ni][e];
         }
       }
 }
@@ -192,10 +206,10 @@ __global__ void __launch_bounds__(GV_THREADS) k_gemv_n_part(int m, int n, const 
       s0[0] += v.x * xs[j];
       s1[0] += v.y * xs[j];
     }
-  } else {
+  } else {  // unaligned rows or the last odd row: scalar loads
     for (; j < nc; j++) {
-      s0[j & 3] += a[(int64_t)j * lda] * xs[j];
-      if (r + 1 < m) s1[j & 3] += a[(int64_t)j * lda + 1] * xs[j];
+      s0[0] += a[(int64_t)j * lda] * xs[j];
+      if (r + 1 < m) s1[0] += a[(int64_t)j * lda + 1] * xs[j];
     }
   }
   part[(int64_t)blockIdx.y * m + r] = (s0[0] + s0[1]) + (s0[2] + s0[3]);
@@ -293,21 +307,53 @@ __global__ void k_dscal(int n, const double* alpha, double* x) {
   if (i < n) x[i] *= *alpha;
 }
 
+// C = alpha sum_z part[z] + beta C (split-K, summed in z order: deterministic)
+__global__ void k_dgemm_splitk_reduce(int M, int N, int S, const double* part, double alpha,
+                                      double beta, double* C, int64_t ldc) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)M * N) return;
+  const int r = (int)(t % M), cc = (int)(t / M);
+  double acc = 0.0;
+  for (int z = 0; z < S; z++) acc += part[((int64_t)z * N + cc) * M + r];
+  double* p = C + r + (int64_t)cc * ldc;
+  *p = beta == 0.0 ? alpha * acc : alpha * acc + beta * *p;
+}
+
 // ---- host wrappers (stream-ordered, column-major, cuBLAS argument order) ----
 
 inline void dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
                   int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                   cudaStream_t s) {
   if (M <= 0 || N <= 0) return;
-  const dim3 grid((unsigned)((M + GM - 1) / GM), (unsigned)((N + GN - 1) / GN));
+  const dim3 grid2((unsigned)((M + GM - 1) / GM), (unsigned)((N + GN - 1) / GN));
+  // Split K when the output has too few tiles to fill the GPU (the reduction's
+  // n x 64 products with K = n): partial blocks in stream-ordered scratch.
+  int S = 1;
+  const long tiles = (long)grid2.x * grid2.y;
+  if (tiles < 296 && K >= 8 * GK) S = (int)std::min<long>((296 + tiles - 1) / tiles, K / (4 * GK));
+  const int kchunk = S > 1 ? ((K + S - 1) / S + GK - 1) / GK * GK : K;
+  S = S > 1 ? (K + kchunk - 1) / kchunk : 1;
+  double* part = nullptr;
+  if (S > 1 && cudaMallocAsync((void**)&part, sizeof(double) * (size_t)S * M * N, s) != cudaSuccess) {
+    part = nullptr;
+    S = 1;
+  }
+  const dim3 grid(grid2.x, grid2.y, (unsigned)S);
+  const int kc = S > 1 ? kchunk : K;
   if (!ta && !tb)
-    k_dgemm<false, false><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    k_dgemm<false, false><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, part);
   else if (!ta && tb)
-    k_dgemm<false, true><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    k_dgemm<false, true><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, part);
   else if (ta && !tb)
-    k_dgemm<true, false><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    k_dgemm<true, false><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, part);
   else
-    k_dgemm<true, true><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    k_dgemm<true, true><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, part);
+  if (part) {
+    const int64_t mn = (int64_t)M * N;
+    k_dgemm_splitk_reduce<<<(unsigned)((mn + 255) / 256), 256, 0, s>>>(M, N, S, part, alpha, beta, C,
+                                                                       ldc);
+    cudaFreeAsync(part, s);
+  }
 }
 
 // y = alpha op(A) x + beta y; part: scratch of ceil(n / 128) * m doubles (no-trans only)

@@ -221,6 +221,16 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
   return 0;
 }
 
+int64_t hsrq_dgemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K,
+                   double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                   double beta, double* C, int64_t ldc, void* stream) {
+  if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+    return HSRQ_ERR_CONFIG;
+  hblas::dgemm(trans_a != 0, trans_b != 0, (int)M, (int)N, (int)K, alpha, A, lda, B, ldb, beta, C,
+               ldc, (cudaStream_t)stream);
+  return cu_ok(cudaGetLastError(), "dgemm") ? 0 : HSRQ_ERR_CUDA;
+}
+
 int64_t hsrq_backmultiply(const double* Q, int64_t ldq, int64_t n, const double* X, int64_t ldx,
                           int64_t ncol, double* Z, int64_t ldz, void* stream_) {
   if (n < 1 || ncol < 0 || ldq < n || ldx < n || ldz < n) return HSRQ_ERR_CONFIG;
