@@ -10,6 +10,7 @@ from conftest import golden
 from test_oracle_golden import hessenberg_checks
 
 pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
 
 
 def test_reduction_matches_reference_golden():
@@ -68,3 +69,35 @@ def test_backmultiply_and_dense_pipeline():
         assert abs(np.linalg.norm(zl) - 1.0) < 1e-12
         r = np.linalg.norm(A @ zl - e * zl) / (af * np.linalg.norm(zl))
         assert r <= 10 * n * np.finfo(float).eps, (l, r)
+
+
+@pytest.mark.parametrize("ta,tb,M,N,K,beta", [
+    (0, 0, 300, 70, 129, 0.0), (0, 1, 257, 190, 64, 1.0), (1, 0, 1000, 64, 3000, 0.0),
+    (1, 1, 33, 17, 5, 0.5), (0, 0, 500, 64, 5000, 0.25), (0, 1, 128, 64, 16, -1.0)])
+def test_front_end_dgemm_matches_fp64_reference(ta, tb, M, N, K, beta):
+    """hsrq_dgemm (the front end's DMMA GEMM, csrc/hsrq_blas.cuh) on ragged
+    shapes, every transpose combination, beta != 0 (accumulator preload) and
+    thin outputs with long K (split-K) vs a torch fp64 product."""
+    import ctypes
+
+    from paper_2101_05063_b200 import _lib
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    L = _lib.load()
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    # column-major r x c matrices stored as row-major (c, r) tensors
+    A = torch.randn((M, K) if ta else (K, M), dtype=torch.float64, device=dev, generator=g)
+    B = torch.randn((K, N) if tb else (N, K), dtype=torch.float64, device=dev, generator=g)
+    C = torch.randn((N, M), dtype=torch.float64, device=dev, generator=g)
+    opA = A if ta else A.t()      # op(A) as a logical M x K tensor
+    opB = B if tb else B.t()      # op(B) as K x N
+    want = -1.5 * (opA @ opB) + beta * C.t()
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    r = L.hsrq_dgemm(ta, tb, M, N, K, -1.5, P(A), A.shape[1], P(B), B.shape[1], beta, P(C), M,
+                     ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert r == 0
+    torch.cuda.synchronize()
+    err = (C.t() - want).abs().max().item()
+    assert err <= 1e-13 * max(1.0, want.abs().max().item()) * max(1, K) ** 0.5, err

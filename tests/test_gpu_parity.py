@@ -318,3 +318,33 @@ def test_budget_solves_match_reference(dev):
             sc = np.max(np.abs(xr[:, l]))
             assert np.max(np.abs(r.x[:, l] - xr[:, l])) <= 1e-12 * sc, (tag, l)
     assert fired >= 12
+
+
+def test_inviter_w_max_grouping_matches_ungrouped(dev):
+    """hsrq3in's w_max grouping (inviter.py:203-239: real groups of 2g, complex
+    groups of g, g = w_max // (2 n N)) on H1 and BASELINE config 1: every
+    column bitwise equal to the ungrouped single-sweep result (columns are
+    independent in every kernel), the golden convergence / restarts, and the
+    reference's Workspace high-water mark (n N cols of the largest group)."""
+    from paper_2101_05063_b200 import ConfigError, InviterConfig, hsrq3in
+
+    g = golden("inviter")
+    for h, eigs, b_r, want_conv in ((g["h1_h"], g["h1_eigs"], 8, g["h1_conv"]),
+                                    (g["c1_h"], g["c1_shifts"], 32, g["c1_conv"])):
+        n = h.shape[0]
+        N = -(-n // b_r)
+        base = hsrq3in(h, eigs, InviterConfig(b_r=b_r, b_c=4))
+        for gsz in (1, 3):
+            w_max = gsz * 2 * n * N
+            r = hsrq3in(h, eigs, InviterConfig(b_r=b_r, b_c=4, w_max=w_max))
+            bits = lambda a: np.ascontiguousarray(a).view(np.float64)  # noqa: E731
+            assert np.array_equal(bits(r.vectors), bits(base.vectors))
+            assert np.array_equal(r.converged, want_conv)
+            assert np.array_equal(r.restarts, base.restarts)
+            assert np.array_equal(r.segment_exp, base.segment_exp)
+            m1 = int(np.count_nonzero(np.asarray(eigs).imag == 0))
+            mc = eigs.size - m1
+            want_peak = max(n * N * min(2 * gsz, m1) if m1 else 0, 2 * n * N * min(gsz, mc) if mc else 0)
+            assert r.peak_crossover_reals == want_peak
+        with pytest.raises(ConfigError):
+            hsrq3in(h, eigs, InviterConfig(b_r=b_r, w_max=2 * n * N - 1))
