@@ -145,9 +145,11 @@ def gather_columns(X_local, counts, group=None, dst=0, out=None):
         for w in (dist.batch_isend_irecv(ops) if ops else []):
             w.wait()
         return Xall
-    if counts[rank]:
+    if counts[rank]:  # the same batched P2P API on both sides (one NCCL group per call)
         peer = dist.get_global_rank(group, dst) if group is not None else dst
-        dist.send(X_local[: counts[rank]].contiguous(), peer, group=group)
+        for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, X_local[: counts[rank]].contiguous(),
+                                                    peer, group=group)]):
+            w.wait()
     return None
 
 
