@@ -272,3 +272,53 @@ def test_config5_all_shifts_residual_and_stratified_oracle(dev, oracle):
             assert d <= 1e-8, (name, int(qq), d)
             Xh[(name, int(qq))] = d
     assert len(Xh) == 80
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_config34_all_shifts_match_oracle(dev, oracle, cfg):
+    """Configs 3 (n = 4000, all 1430 complex shifts Im > 0) and 4 (n = 2000
+    graded, 602 real + 699 complex shifts perturbed by 1e-14) in full, b_r =
+    128, one sweep of every shift vs the oracle on the same start vector:
+    segment exponents exact (tile 0 +-1), vectors phase-aligned to 1e-8,
+    residual <= 10 n eps on every column, the same convergence decisions."""
+    import instances
+    from paper_2101_05063_b200 import solver
+
+    h = instances.make_h(cfg)
+    sel = instances.shifts(cfg)
+    er = sel[sel.imag == 0].real
+    ec = sel[sel.imag > 0]
+    n, b_r = h.shape[0], 128
+    rho = np.finfo(float).eps * np.max(np.sum(np.abs(h), axis=1))
+    start = rho * np.ones(n)
+    out, _ = solver.solve_group(h, ec, er, start, b_r)
+    assert out.nfail == 0
+    threads = os.cpu_count() or 1
+    parts = []
+    if ec.size:
+        parts.append(oracle.solve(h, ec, np.repeat(start[:, None], ec.size, 1).astype(complex), b_r,
+                                  b_c=8, mode="eigvec", nthreads=threads))
+    if er.size:
+        parts.append(oracle.solve(h, er, np.repeat(start[:, None], er.size, 1), b_r, b_c=8,
+                                  mode="eigvec", nthreads=threads))
+    want = np.concatenate([p.segment_exp for p in parts], axis=1)
+    seg = out.seg_exp.cpu().numpy()
+    assert np.array_equal(seg[1:], want[1:])
+    assert np.max(np.abs(seg[0] - want[0])) <= 1
+    X = out.X.cpu().numpy()
+    mc = ec.size
+    refs = np.concatenate([p.x for p in parts], axis=1)
+    lams = np.concatenate([ec, er.astype(complex)])
+    V = np.empty((n, lams.size), dtype=complex)
+    V[:, :mc] = (X[0:2 * mc:2] + 1j * X[1:2 * mc:2]).T
+    V[:, mc:] = X[2 * mc:].T
+    ip = np.sum(V.conj() * refs, axis=0)
+    ph = np.where(ip != 0, ip / np.abs(ip), 1.0)
+    dev_err = np.linalg.norm(V * ph[None, :] - refs, axis=0)
+    assert dev_err.max() <= 1e-8, (dev_err.max(), int(dev_err.argmax()))
+    hf = np.linalg.norm(h, "fro")
+    res = np.linalg.norm(h @ V - V * lams[None, :], axis=0) / (hf * np.linalg.norm(V, axis=0))
+    assert res.max() <= 10 * n * np.finfo(float).eps, res.max()
+    l2 = out.log2norm.cpu().numpy()
+    l2w = np.concatenate([p.log2norm for p in parts])
+    assert np.array_equal(solver.converged_log2(l2, n), solver.converged_log2(l2w, n))

@@ -33,10 +33,17 @@ for W in (int(w) for w in sys.argv[1:]):
     gs = GroupSolver(dh, b_r, my_c.size, my_r.size)
     gs.set_shifts(my_c, my_r)
     gs.launch(start, True)
+    graph = os.environ.get("HSRQ_GRAPH") == "1"  # replay the sweep as one CUDA graph
+    if graph:
+        gs.capture(start, True)
+        gs.replay()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(2):
-        gs.launch(start, True, sync=False)
+        if graph:
+            gs.replay(sync=False)
+        else:
+            gs.launch(start, True, sync=False)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 2
