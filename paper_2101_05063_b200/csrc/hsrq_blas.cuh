@@ -284,6 +284,71 @@ __global__ void k_trmm_ru(int rows, int p, const double* T, int64_t ldt, double*
   }
 }
 
+// The panel's fused column kernels (one launch where the unfused sequence
+// needed two or three; the reduction is launch-bound per column):
+//
+// k_gemv_t_trmv: y = A^T x (one CTA per column, as k_gemv_t), and the CTA
+// that finishes last (a device counter) then forms z = s op(T) y for the
+// panel's triangular factor T (p x p upper, p <= 64): trans = 1 -> z = T^T y
+// (the left update's u), trans = 0 -> z = T y (the T column); s = *scale (a
+// device scalar, e.g. -tau) or 1 when scale is NULL.  z may alias y.
+__global__ void __launch_bounds__(256) k_gemv_t_trmv(int m, int n, const double* A, int64_t lda,
+                                                     const double* x, double* y, const double* T,
+                                                     int64_t ldt, int trans, const double* scale,
+                                                     double* z, unsigned* counter) {
+  __shared__ double red[8];
+  __shared__ bool last;
+  const int col = blockIdx.x;
+  const double* a = A + (int64_t)col * lda;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < m; i += 256) s += a[i] * x[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; w++) t += red[w];
+    y[col] = t;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == (unsigned)n - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double ys[64];
+  if (threadIdx.x < n) ys[threadIdx.x] = y[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < n) {
+    const int i = threadIdx.x;
+    double acc = 0.0;
+    if (!trans) {
+      for (int j = i; j < n; j++) acc += T[i + (int64_t)j * ldt] * ys[j];
+    } else {
+      for (int j = 0; j <= i; j++) acc += T[j + (int64_t)i * ldt] * ys[j];
+    }
+    z[i] = scale ? *scale * acc : acc;
+  }
+  if (threadIdx.x == 0) *counter = 0u;  // ready for the next column
+}
+
+// y = tau * (sum_c part[c] - Y[:, :p] w): the Av GEMV's chunk reduction fused
+// with the panel correction and the reflector's scale (DLAHR2's Y column).
+__global__ void k_gemv_n_reduce_y(int m, int nchunk, const double* part, const double* Y,
+                                  int64_t ldy, int p, const double* w, const double* tau,
+                                  double* y) {
+  __shared__ double ws[64];
+  if (threadIdx.x < p) ws[threadIdx.x] = w[threadIdx.x];
+  __syncthreads();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  double s = 0.0;
+#pragma unroll 8
+  for (int c = 0; c < nchunk; c++) s += part[(int64_t)c * m + r];
+  double cor = 0.0;
+  for (int k = 0; k < p; k++) cor += Y[r + (int64_t)k * ldy] * ws[k];
+  y[r] = *tau * (s - cor);
+}
+
 // x = T x (trans = 0) or T^T x (trans = 1), T p x p upper (ldt), one block.
 __global__ void k_trmv_u(int p, const double* T, int64_t ldt, double* x, int trans) {
   __shared__ double xs[64];

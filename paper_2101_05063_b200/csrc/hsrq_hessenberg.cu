@@ -139,8 +139,8 @@ const char* hsrq_hessenberg_last_error(void) { return g_herr; }
 size_t hsrq_hessenberg_workspace_bytes(int64_t n) {
   const size_t nb = HB_NB;
   const size_t nchunk = ((size_t)n + hblas::GV_COLS - 1) / hblas::GV_COLS;
-  return sizeof(double) * ((size_t)n * nb * 2 + nb * nb + 4 * nb + nb * (size_t)n + 256 +
-                           nchunk * (size_t)n);
+  return sizeof(double) * ((size_t)n * nb * 2 + nb * nb + 5 * nb + nb * (size_t)n + 256 +
+                           nchunk * (size_t)n + 8);
 }
 
 int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, int64_t n,
@@ -157,6 +157,9 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
   double* u = ntau + nb;                // nb
   double* W = u + nb;                   // n x nb (W^T of the left update; Q V T)
   double* part = W + (size_t)nb * n + 256;  // GEMV partial sums
+  double* wv = u + nb;                      // V^T v of the current column (raw), nb
+  unsigned* counter = (unsigned*)(part + ((size_t)n + hblas::GV_COLS - 1) / hblas::GV_COLS * (size_t)n);
+  if (!cu_ok(cudaMemsetAsync(counter, 0, sizeof(unsigned), stream), "counter")) return HSRQ_ERR_CUDA;
   if (Q) {
     k_set_identity<<<(unsigned)((n * n + 255) / 256), 256, 0, stream>>>(Q, n, ldq);
     if (!cu_ok(cudaGetLastError(), "identity")) return HSRQ_ERR_CUDA;
@@ -173,9 +176,9 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
       if (i > 0) {
         // right update of column j: a_j -= Y[:, :i] V[j, :i]^T
         dgemv(false, (int)n, i, -1.0, Y, n, V + j, n, 1.0, aj, part, stream);
-        // left update of rows j0+1.. : a -= V T^T V^T a
-        dgemv(true, (int)L, i, 1.0, V + j0 + 1, n, aj + j0 + 1, 1, 0.0, u, part, stream);
-        k_trmv_u<<<1, 64, 0, stream>>>(i, T, nb, u, 1);
+        // left update of rows j0+1.. : a -= V T^T V^T a  (u = T^T V^T a in one launch)
+        k_gemv_t_trmv<<<(unsigned)i, 256, 0, stream>>>((int)L, i, V + j0 + 1, n, aj + j0 + 1, u, T,
+                                                       nb, 1, nullptr, u, counter);
         dgemv(false, (int)L, i, -1.0, V + j0 + 1, n, u, 1, 1.0, aj + j0 + 1, part, stream);
       }
       double* vi = V + (size_t)i * n;
@@ -184,16 +187,20 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
       if (!cu_ok(cudaGetLastError(), "reflector")) return HSRQ_ERR_CUDA;
       // Y[:, i] = tau (A[:, j+1:] v - Y[:, :i] (V^T v)); T[:i, i] = -tau T[:i, :i] (V^T v)
       double* yi = Y + (size_t)i * n;
-      dgemv(false, (int)n, (int)(n - j - 1), 1.0, A + (j + 1) * lda, lda, vi + j + 1, 1, 0.0, yi,
-            part, stream);
-      if (i > 0) {
-        double* ti = T + (size_t)i * nb;
-        dgemv(true, (int)L, i, 1.0, V + j0 + 1, n, vi + j0 + 1, 1, 0.0, ti, part, stream);
-        dgemv(false, (int)n, i, -1.0, Y, n, ti, 1, 1.0, yi, part, stream);
-        k_trmv_u<<<1, 64, 0, stream>>>(i, T, nb, ti, 0);
-        k_dscal<<<1, 64, 0, stream>>>(i, ntau + i, ti);
+      if (i > 0)  // w = V^T v (kept raw for Y) and the T column, one launch
+        k_gemv_t_trmv<<<(unsigned)i, 256, 0, stream>>>((int)L, i, V + j0 + 1, n, vi + j0 + 1, wv,
+                                                       T, nb, 0, ntau + i, T + (size_t)i * nb,
+                                                       counter);
+      {  // A[:, j+1:] v, reduced in chunk order with the Y correction and tau fused
+        const int nv = (int)(n - j - 1);
+        const int nchunk = (nv + GV_COLS - 1) / GV_COLS;
+        if (nchunk > 0)
+          k_gemv_n_part<<<dim3((unsigned)((n + GV_ROWS - 1) / GV_ROWS), (unsigned)nchunk),
+                          GV_THREADS, 0, stream>>>((int)n, nv, A + (j + 1) * lda, lda, vi + j + 1,
+                                                   1, part);
+        k_gemv_n_reduce_y<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(
+            (int)n, nchunk, part, Y, n, i, wv, tau + i, yi);
       }
-      k_dscal<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>((int)n, tau + i, yi);
     }
     const int64_t c0 = j0 + pb, nc = n - c0;  // trailing columns
     if (nc > 0) {
