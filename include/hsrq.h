@@ -253,6 +253,9 @@ int32_t hsrq_tune_diag(int32_t dp, int32_t dwr, int32_t dwc, int32_t wsr, int32_
  * 8 per CTA, where the automatic choice is 32 lanes per shift).  Results
  * are bit-identical either way. */
 int32_t hsrq_tune_diag_rx(int32_t np);
+/* Panel form for b_r = 128: 1 = 2-CTA clusters of 64-row CTAs (k_panel_cl,
+ * default), 0 = one 128-row CTA per tile row (k_panel).  Bit-identical. */
+int32_t hsrq_tune_panel(int32_t cluster);
 
 /*
  * Tile-level entry points (parity tests against the reference kernels).

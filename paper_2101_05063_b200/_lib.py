@@ -62,6 +62,7 @@ SIGNATURES = {
     "hsrq_set_timing": (None, [_i32]),
     "hsrq_tune_diag": (_i32, [_i32, _i32, _i32, _i32, _i32]),
     "hsrq_tune_diag_rx": (_i32, [_i32]),
+    "hsrq_tune_panel": (_i32, [_i32]),
     "hsrq_phase_times": (None, [_p]),
     "hsrq_tile_diag": (
         _i64,

@@ -25,6 +25,7 @@
 //   k_backtransform  rbacktransform / crbacktransform (:326-375, :759-822).
 //
 // Scale factors are carried as int32 log2 exponents (see include/hsrq.h).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -257,6 +258,7 @@ __global__ void k_zero_bop(double* Bop, int64_t count) {
 #include "hsrq_diag_rx.cuh"
 
 #include "hsrq_panel.cuh"
+#include "hsrq_panel_cl.cuh"
 
 #include "hsrq_backtransform.cuh"
 
@@ -383,6 +385,7 @@ bool ck(cudaError_t e, const char* what) {
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 int g_panel_fast = 1;  // HSRQ_PANEL_FAST=0 forces the general epilogue (testing)
+int g_panel_cluster = 1;  // HSRQ_PANEL_CLUSTER=0: the 256-thread k_panel fast path instead of k_panel_cl
 
 // Diagonal-kernel variants: DP lanes per shift and DW warps per CTA, chosen
 // per kind (real / complex) from the number of shifts in the launch.  The
@@ -449,6 +452,7 @@ bool diag_attrs() {
 #endif
   const char* pf = getenv("HSRQ_PANEL_FAST");
   if (pf) g_panel_fast = atoi(pf);
+  if (const char* pcl = getenv("HSRQ_PANEL_CLUSTER")) g_panel_cluster = atoi(pcl);
   const char* pp = getenv("HSRQ_PANEL_PREFETCH");
   if (pp) {
     int v = atoi(pp);
@@ -702,7 +706,9 @@ int64_t ensure_attrs() {
         !ck(cudaFuncSetAttribute(k_panel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)panel_smem), "attr panel") ||
         !ck(cudaFuncSetAttribute(k_panel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)panel_smem), "attr panel fast"))
+                                 (int)panel_smem), "attr panel fast") ||
+        !ck(cudaFuncSetAttribute(k_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(PanelClSmem)), "attr panel cluster"))
       return HSRQ_ERR_CUDA;
     attr_done[cur_dev] = true;
   }
@@ -959,6 +965,33 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     p.t0 = t0;
     p.t1 = t1;
     const Ctx& cj = cb[jt & 1];
+    if (const char* e = getenv("HSRQ_PANEL_EXP")) {  // diagnostics: 64-row 4-warp GEMM only
+      const int st = atoi(e);
+      dim3 g64((unsigned)(2 * (t1 - t0)), (unsigned)(c.ncol_pad / BN));
+      if (st == 3) {
+        static bool a3 = false;
+        if (!a3) cudaFuncSetAttribute(k_panel64_gemm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(Gemm64Smem<3>));
+        a3 = true;
+        k_panel64_gemm<3><<<g64, 128, sizeof(Gemm64Smem<3>), stream>>>(cj, p);
+      } else {
+        static bool a2 = false;
+        if (!a2) cudaFuncSetAttribute(k_panel64_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(Gemm64Smem<2>));
+        a2 = true;
+        k_panel64_gemm<2><<<g64, 128, sizeof(Gemm64Smem<2>), stream>>>(cj, p);
+      }
+      g_launches++;
+      return;
+    }
+    // b_r = 128 with full K chunks: the 2-CTA cluster form (HSRQ_PANEL_CLUSTER=0: k_panel)
+    if (a16 && b_r == BM && g_panel_fast && g_panel_cluster && p.k == BM && !c.diag_gemm_only &&
+        !c.diag_tl) {
+      dim3 gcl((unsigned)(2 * (t1 - t0)), (unsigned)(c.ncol_pad / BN));
+      k_panel_cl<<<gcl, CL_THREADS, sizeof(PanelClSmem), stream>>>(cj, p, rsc);
+      g_launches++;
+      return;
+    }
     dim3 gp((unsigned)((t1 - t0 + S - 1) / S), (unsigned)(c.ncol_pad / BN));
     if (a16 && b_r == BM && g_panel_fast)
       k_panel<true, true, true><<<gp, PANEL_THREADS, panel_smem, stream>>>(cj, p, rsc);
@@ -1455,6 +1488,11 @@ int32_t hsrq_tune_diag(int32_t dp, int32_t dwr, int32_t dwc, int32_t wsr, int32_
   g_diag_ws_r = wsr;
   g_diag_ws = wsc;
   return 0;
+}
+int32_t hsrq_tune_panel(int32_t cluster) {
+  diag_attrs();  // reads the environment once; the explicit setting wins
+  g_panel_cluster = cluster != 0;
+  return g_panel_cluster;
 }
 int32_t hsrq_tune_diag_rx(int32_t np) {
   diag_attrs();  // reads the environment once; the explicit setting wins

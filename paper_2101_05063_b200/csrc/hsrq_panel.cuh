@@ -1135,3 +1135,82 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
     tlp_[4] = g;
   }
 }
+
+// ---------------------------------------------------------------------------
+// Diagnostics (HSRQ_PANEL_EXP=S, wrong results): the panel GEMM alone with
+// 64-row, 4-warp CTAs and S cp.async stages -- the main loop of a cluster
+// design (two CTAs per tile row) measured before building it.
+template <int ST>
+struct Gemm64Smem {
+  double A[ST][BK][64 + 4];
+  double B[ST][2 * BN][BPAD];
+};
+template <int ST>
+__global__ void __launch_bounds__(128, 4) k_panel64_gemm(Ctx c, PanelArgs p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Gemm64Smem<ST>& sm = *reinterpret_cast<Gemm64Smem<ST>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t row0 = (int64_t)(p.t0 * 2 + blockIdx.x) * 64;
+  const int64_t col0 = (int64_t)blockIdx.y * BN;
+  const int nk = p.k / BK;
+  // A: 16 x 64 per chunk = 512 16-byte copies, 4 per thread; B: 64 x 16 = 512, 4 per thread
+  const int kk0 = tid / 32, m2 = (tid % 32) * 2;
+  const double* a0 = c.H + (p.js - 1 + kk0) * c.ldh + row0 + m2;
+  const int nn = tid / 8, k2 = (tid % 8) * 2;
+  const double* b0 = c.Bop + (2 * col0 + nn) * KP + k2;
+  auto load = [&](int stage, int kc) {
+    const double* a = a0 + (int64_t)kc * BK * c.ldh;
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      cp_async16(&sm.A[stage][kk0 + 4 * i][m2], a + (int64_t)4 * i * c.ldh, true);
+    const double* b = b0 + kc * BK;
+#pragma unroll
+    for (int i = 0; i < 4; i++) cp_async16(&sm.B[stage][nn + 16 * i][k2], b + 16 * i * KP, true);
+  };
+#pragma unroll
+  for (int s = 0; s < ST - 1; s++) {
+    if (s < nk) load(s, s);
+    cp_commit();
+  }
+  const int wm = warp & 1, wn = warp >> 1;
+  const int g = lane >> 2, t4 = lane & 3;
+  double acc[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
+  for (int kc = 0; kc < nk; kc++) {
+    cp_wait<ST - 2>();
+    __syncthreads();
+    if (kc + ST - 1 < nk) load((kc + ST - 1) % ST, kc + ST - 1);
+    cp_commit();
+    const int st = kc % ST;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[2][2], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++) {
+        const int r = wm * 32 + mi * 16 + g;
+        af[mi][0] = sm.A[st][kk + t4][r];
+        af[mi][1] = sm.A[st][kk + t4][r + 8];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ni++) bf[ni] = sm.B[st][wn * 32 + ni * 8 + g][kk + t4];
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 4; ni++) mma_f64(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+    }
+  }
+  cp_wait<0>();
+  double sum = 0.0;  // every accumulator live (otherwise the MMAs are dead code)
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) sum += acc[i][j][e];
+  if (sum == 1.2345e-300) c.X[0] = sum;
+}

@@ -257,3 +257,37 @@ def test_production_selection_at_scale_is_variant_invariant(dev, lib):
     _same(outs[0], outs[1], "auto vs DP32/G32")
     _same(outs[0], outs[2], "auto vs DP8/G16")
     _same(outs[0], outs[3], "auto vs rotation-ahead DP16 pairs/G32")
+
+
+@pytest.mark.parametrize("n,seed,rhs,nr,nc,la", [
+    (1000, 4, 1e300, 10, 14, "0"), (700, 1, 1.0, 9, 12, "1"), (1300, 6, 1e300, 30, 40, "0"),
+    (640, 3, 1e300, 5, 6, "1")])
+def test_panel_cluster_form_is_bitwise_the_single_cta_form(dev, lib, monkeypatch, n, seed, rhs, nr,
+                                                           nc, la):
+    """k_panel_cl (a tile row over a 2-CTA cluster, maxima exchanged through
+    distributed shared memory) vs k_panel's fast path, b_r = 128, guards
+    firing (rhs 1e300), lookahead on / off, eigvec and solve modes: bitwise."""
+    from paper_2101_05063_b200.core import HessenbergMatrix
+    from paper_2101_05063_b200.solver import DeviceHessenberg, GroupSolver
+
+    monkeypatch.setenv("HSRQ_LOOKAHEAD", la)
+    h, er, ec = _case(n, seed, nr, nc)
+    rho = np.finfo(float).eps * np.max(np.sum(np.abs(h), axis=1))
+    dh = DeviceHessenberg(HessenbergMatrix(h), dev)
+    rng = np.random.default_rng(seed)
+    cases = [(torch.full((n,), rho if rhs == 1.0 else rhs, dtype=torch.float64, device=dev), True,
+              "eigvec"),
+             (torch.from_numpy(rng.standard_normal((2 * ec.size + er.size, n))).to(dev), False,
+              "solve")]
+    try:
+        for B, bc, mode in cases:
+            outs = []
+            for cl in (0, 1):
+                lib.hsrq_tune_panel(cl)
+                gs = GroupSolver(dh, 128, ec.size, er.size)
+                gs.set_shifts(ec + (0.125j if mode == "solve" else 0), er + (0.125 if mode == "solve" else 0))
+                assert gs.launch(B, bc, mode=mode) == 0
+                outs.append(_outputs(gs))
+            _same(outs[0], outs[1], f"panel cluster {mode}")
+    finally:
+        lib.hsrq_tune_panel(1)
