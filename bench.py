@@ -509,7 +509,8 @@ def run_gpu(args):
 
     peak, peak_src, hbm = load_peaks()
     traffic, traffic_note = None, None
-    prof = os.path.join(ROOT, "profiles", "ncu_r01_k_panel_cfg5_jt84.json")
+    prof_rel = "profiles/ncu_r02_k_panel_cl_cfg5_jt84.json"
+    prof = os.path.join(ROOT, prof_rel)
     if os.path.exists(prof) and n == 16000:
         with open(prof) as f:
             pj = json.load(f)
@@ -518,7 +519,7 @@ def run_gpu(args):
         traffic = rd + wr
         traffic_note = {"launch": pj["launch"], "algorithmic_bytes": pj["algorithmic_bytes"],
                         "ratio": traffic / pj["algorithmic_bytes"],
-                        "source": "profiles/ncu_r01_k_panel_cfg5_jt84.json (ncu --set full)"}
+                        "source": prof_rel + " (ncu --set full)"}
     nvec = m_total_r + m_total_c
     ref_fl = F.reference_flops(n, b_r, m_total_r, m_total_c)
     exe_fl = F.executed_flops(n, b_r, m_total_r, m_total_c)
@@ -551,13 +552,13 @@ def run_gpu(args):
         "phase_ms": {"diag": phase[0], "scalars": phase[4], "panel": phase[1],
                      "backtransform": phase[2], "setup": phase[3]},
         "roofline": {
-            "bound": "tensor", "kernel": "k_panel (DMMA f64)",
+            "bound": "tensor", "kernel": "k_panel_cl / k_panel (DMMA f64 panel update)",
             "achieved": ach, "peak": peak, "unit": "TFLOP/s",
             "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_detail": traffic_note,
             "peak_source": peak_src,
             "executed_achieved": my_exe / (panel_ms / 1e3) / 1e12 if panel_ms > 0 else None,
             "algorithmic": "reference flop model (hessrq flops.py) ReduceOffdiag+Update flops of "
-                           "the panel launches / summed k_panel event time",
+                           "the panel launches / summed panel-kernel event time",
         },
         "gpu_launches": launches,
         "failed_shifts": int(nf),

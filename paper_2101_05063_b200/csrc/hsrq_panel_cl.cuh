@@ -23,6 +23,9 @@ constexpr int CL_THREADS = 128;           // 4 warps: 2 (M) x 2 (N) warp tiles o
 constexpr int CL_STAGES = 2;
 constexpr int CL_ROWS = 8;                // epilogue: threads per column pair
 constexpr int CL_RPT = CL_BM / CL_ROWS;   // rows per thread (8)
+#ifndef CL_MINB
+#define CL_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
 
 struct PanelClSmem {
   union {
@@ -41,7 +44,7 @@ struct PanelClSmem {
   int need[BN];
 };
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CL_THREADS, 4)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CL_THREADS, CL_MINB)
     k_panel_cl(Ctx c, PanelArgs p, const RowScalars* __restrict__ RSc) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PanelClSmem& sm = *reinterpret_cast<PanelClSmem*>(smem_raw);
