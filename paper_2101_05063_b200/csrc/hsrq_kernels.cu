@@ -27,6 +27,7 @@
 // Scale factors are carried as int32 log2 exponents (see include/hsrq.h).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <vector>
@@ -39,6 +40,23 @@
 
 #include "../../include/hsrq.h"
 #include "hsrq_device.cuh"
+
+namespace {
+// NVTX range over a host enqueue region (one range per
+// solve, per tile-column step, per backtransform).  Without a profiler
+// attached nvtxRangePush is a no-op call.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* fmt, int v) {
+    char buf[64];
+    snprintf(buf, sizeof(buf), fmt, v);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 using namespace hsrq;
 
@@ -723,6 +741,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
                    size_t ws_bytes, cudaStream_t stream, const HostFeed* feed = nullptr,
                    double omega_in = 0.0) {
   g_launches = 0;
+  NvtxRange nv_solve("hsrq solve_group");
   if (n < 1 || b_r < 1 || b_r > MAXK || b_r > n || mc < 0 || mr < 0 || mc + mr < 1 || ldx < n ||
       ldh < n || ldc < n) {
     snprintf(g_err, sizeof(g_err), "bad configuration (n=%lld b_r=%d)", (long long)n, b_r);
@@ -1012,8 +1031,12 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   int stop_at = -1;
   if (const char* e = getenv("HSRQ_STOP_AT")) stop_at = atoi(e);
   bool stopped = stop_at == c.N - 1 && c.N - 1 == 0;
-  run_diag(c.N - 1, stream, side);
+  {
+    NvtxRange nv("hsrq diag tile %d", c.N - 1);
+    run_diag(c.N - 1, stream, side);
+  }
   for (int jt = c.N - 1; jt >= 1 && !stopped; --jt) {
+    NvtxRange nv("hsrq tile column %d", jt);
     PanelArgs p;
     p.jt = jt;
     p.js = (int64_t)jt * b_r;
@@ -1050,6 +1073,7 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
     }
   }
   if (g_timing) cudaEventRecord(ev[nev - 3], stream);
+  NvtxRange nv_bt("hsrq backtransform");
   if (stopped) {
     // (timing of a stopped sweep is not recorded)
   } else if (!feed || !feed->X_host) {
