@@ -375,6 +375,31 @@ def run_gpu(args):
     ms = float(t_local.item())
     phase /= args.steps
 
+    # ---- roofline pass: the same K steps with the lookahead off, so each panel
+    # launch runs alone on the GPU (with the lookahead the diagonal sweep of the
+    # next column shares the SMs with the panel, and the panel's event times
+    # include it); the timed region above is the one `value` reports ----
+    phase_serial = np.zeros(5)
+    ms_serial = None
+    if not args.no_serial_pass:
+        os.environ["HSRQ_LOOKAHEAD"] = "0"
+        try:
+            step()
+            torch.cuda.synchronize()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(args.steps):
+                step(timing=True)
+            s1.record(stream)
+            torch.cuda.synchronize()
+            lib.hsrq_phase_times(ctypes.c_void_p(phase_serial.ctypes.data))
+            phase_serial /= args.steps
+            ms_serial = s0.elapsed_time(s1) / args.steps
+        finally:
+            del os.environ["HSRQ_LOOKAHEAD"]
+            lib.hsrq_set_timing(0)
+
     # ---- e2e through the C ABI with host (pinned) buffers: hsrq_solve_group_host,
     # the reference's calling convention (numpy in/out); H streams to the device
     # in column blocks overlapped with the sweep, X and the scale factors return ----
@@ -528,7 +553,7 @@ def run_gpu(args):
     N = (n + b_r - 1) // b_r
     pan_alg = my_ref_fl - (my_r.size * (F.per_shift_flops(n, b_r, False) - _offdiag_update(n, b_r, False))
                            + my_c.size * (F.per_shift_flops(n, b_r, True) - _offdiag_update(n, b_r, True)))
-    panel_ms = phase[1]
+    panel_ms = phase_serial[1] if ms_serial is not None else phase[1]
     ach = pan_alg / (panel_ms / 1e3) / 1e12 if panel_ms > 0 else None
     my_exe = F.executed_flops(n, b_r, my_r.size, my_c.size)
     line = {
@@ -550,7 +575,15 @@ def run_gpu(args):
         "executed_tflops": exe_fl / (ms / 1e3) / 1e12,
         "eigenvectors_incl_conjugates_per_s": (m_total_r + 2 * m_total_c) / (ms / 1e3),
         "phase_ms": {"diag": phase[0], "scalars": phase[4], "panel": phase[1],
-                     "backtransform": phase[2], "setup": phase[3]},
+                     "backtransform": phase[2], "setup": phase[3],
+                     "note": "timed region (lookahead on: the diag sweep of column jt-1 runs "
+                             "beside panel jt, so diag and panel overlap)"},
+        "phase_ms_serial": ({"diag": phase_serial[0], "scalars": phase_serial[4],
+                             "panel": phase_serial[1], "backtransform": phase_serial[2],
+                             "setup": phase_serial[3], "ms_per_step": ms_serial,
+                             "note": "second K-step pass with HSRQ_LOOKAHEAD=0 (phases "
+                                     "serialised); the roofline is taken from it"}
+                            if ms_serial is not None else None),
         "roofline": {
             "bound": "tensor", "kernel": "k_panel_cl / k_panel (DMMA f64 panel update)",
             "achieved": ach, "peak": peak, "unit": "TFLOP/s",
@@ -559,6 +592,8 @@ def run_gpu(args):
             "executed_achieved": my_exe / (panel_ms / 1e3) / 1e12 if panel_ms > 0 else None,
             "algorithmic": "reference flop model (hessrq flops.py) ReduceOffdiag+Update flops of "
                            "the panel launches / summed panel-kernel event time",
+            "measured_in": ("phase_ms_serial pass (K steps, lookahead off: each panel launch alone "
+                            "on the GPU)" if ms_serial is not None else "timed region"),
         },
         "gpu_launches": launches,
         "failed_shifts": int(nf),
@@ -658,6 +693,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-shards", action="store_true", help="skip the 2/4/8-way shard projection")
+    ap.add_argument("--no-serial-pass", action="store_true",
+                    help="skip the lookahead-off pass the roofline is taken from")
     ap.add_argument("--cpu-real", type=int, default=16)
     ap.add_argument("--cpu-cplx", type=int, default=16)
     ap.add_argument("--ref-real", type=int, default=8, help="reference arm: real shifts per step")

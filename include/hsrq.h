@@ -219,7 +219,7 @@ int64_t hsrq_solve_group_host_async(const double* H, int64_t ldh, int64_t n, int
                                     size_t dev_ws_bytes, void* stream);
 int64_t hsrq_host_wait(int64_t ticket);
 
-/* Guard-path event counters (diagnostics): out_host[16]; reset != 0 zeroes them. */
+/* Guard-path event counters (diagnostics): out_host[32]; reset != 0 zeroes them. */
 int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset);
 /* Diagnostics build -DHSRQ_STEPPROF only (returns 0 otherwise): per-phase
  * clock64 sums of the complex diagonal sweep's steps ([0..9]) and the number

@@ -709,6 +709,22 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
       tx = gmax<DP>(tx);
       bool full = false;
       int e = 0;
+#ifdef HSRQ_COUNTERS
+      // what-if: which tighter cheap bounds would have passed the guard-2 test
+      if (exact2 && pl == 0 && tx > 0.0 && tr > 0.0) {
+        const double xbm = sqrt(tx) * p2(ex) * (1.0 + 0x1p-40);
+        const double rbm = sqrt(tr) * p2(er) * (1.0 + 0x1p-40);
+        const double ax1 = (fabs(xk.re) + fabs(xk.im)) * DSLACK, axm = cabs_(xk);
+        if (protect_update_is_one(xbm, rb, ax1, omega)) HSRQ_COUNT(16);
+        if (protect_update_is_one(xb * DSLACK, rbm, ax1, omega)) HSRQ_COUNT(17);
+        if (protect_update_is_one(xbm, rbm, ax1, omega)) HSRQ_COUNT(18);
+        if (protect_update_is_one(xbm, rbm, axm, omega)) HSRQ_COUNT(19);
+        if (protect_update_is_one(xb * DSLACK, rb, axm, omega)) HSRQ_COUNT(20);
+        if (xbm > omega) HSRQ_COUNT(22);
+        if (rbm * axm > omega) HSRQ_COUNT(23);
+        if (axm > 1.0) HSRQ_COUNT(24);
+      }
+#endif
       if (exact2) {
         const double ax = cabs_(xk);
         if (ex > -1000 && ex < 1020 && er > -1000 && er < 1020 && tx >= 0x1p-960 &&
@@ -743,6 +759,9 @@ __global__ void __launch_bounds__(DW * 32) k_diag_cplx(Ctx c, DiagArgs a) {
         bm = gmax<DP>(bm);
         if (full) e = protect_update_e(bm, rm, cabs_(xk), omega);
       }
+#ifdef HSRQ_COUNTERS
+      if (exact2 && e == 0 && pl == 0) HSRQ_COUNT(21);
+#endif
       if (exact2 && e < 0) {
         if (pl == 0) HSRQ_COUNT(5);
         const cplx xi = mk(p2(e), 0.0);

@@ -79,7 +79,7 @@ constexpr int KP = 128;      // stride of the B operand (K padded)
 __device__ __constant__ int g_panel_prefetch = 1;
 
 // Event counters (guard paths taken), read with hsrq_debug_counters().
-__device__ unsigned long long g_ctr[16];
+__device__ unsigned long long g_ctr[32];
 #ifdef HSRQ_COUNTERS
 #define HSRQ_COUNT(i) atomicAdd(&g_ctr[(i)], 1ULL)
 #else
@@ -898,16 +898,14 @@ int64_t solve_impl(const double* H, int64_t ldh, int64_t n, int32_t b_r, const d
   }
   // Lookahead: the diagonal sweep of column jt-1 only needs tile row jt-1 of
   // panel jt, so that row goes first and the sweep overlaps the rest of the
-  // panel.  It pays when the sweep leaves room on the SMs (few shifts per
-  // GPU, i.e. a rank's shard); with all of config 5 on one GPU the sweep's
-  // shared memory fills every SM and the two phases serialise anyway.
-  // HSRQ_LOOKAHEAD=0/1 forces it off/on.
+  // panel.  HSRQ_LOOKAHEAD=0/1 forces it off/on (default on).
   // Measured (tools/shard_time.py, config-5 shards, ms per solve, off -> on):
-  // 1 GPU 515 -> 514, 1/2 shard 291 -> 261, 1/4 175 -> 162, 1/8 116 -> 105.
-  // Off for a whole config-5 group: with the warp-pair sweep it gains 1.4 %
-  // there (485 -> 478 ms) but the panel's launch times (the roofline's
-  // denominator) would then include the concurrent sweep (panel 335 -> 433 ms).
-  bool lookahead = c.ms <= 6000;
+  // 1 GPU 515 -> 514, 1/2 shard 291 -> 261, 1/4 175 -> 162, 1/8 116 -> 105
+  // (round 1); with the 2-CTA cluster panel, all of config 5 on one GPU:
+  // 464.0 -> 452.3 ms (tools/profile_solve.py).  The panel's launch times
+  // then include the concurrent sweep, so bench.py takes the roofline from a
+  // second timed pass with HSRQ_LOOKAHEAD=0.
+  bool lookahead = true;
   if (const char* e = getenv("HSRQ_LOOKAHEAD")) lookahead = atoi(e) != 0;
   // Bop / SS are double-buffered by column parity: the lookahead sweep of
   // jt-1 writes its panel operands while panel jt still reads its own.
@@ -1493,11 +1491,11 @@ int64_t hsrq_debug_stepprof(int64_t* out_host, int32_t reset) {
 }
 
 int64_t hsrq_debug_counters(int64_t* out_host, int32_t reset) {
-  unsigned long long v[16];
+  unsigned long long v[32];
   if (cudaMemcpyFromSymbol(v, g_ctr, sizeof(v)) != cudaSuccess) return HSRQ_ERR_CUDA;
-  for (int i = 0; i < 16; i++) out_host[i] = (int64_t)v[i];
+  for (int i = 0; i < 32; i++) out_host[i] = (int64_t)v[i];
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[32] = {0};
     if (cudaMemcpyToSymbol(g_ctr, z, sizeof(z)) != cudaSuccess) return HSRQ_ERR_CUDA;
   }
   return 0;

@@ -182,6 +182,9 @@ __device__ __forceinline__ bool scalars_step2_is_one(const Ctx& c, int jt, int i
   return protect_update_is_one(xbound, c.RS[(int64_t)jt * c.N + it], zmax, c.omega);
 }
 
+#ifndef SCAL_ITEM_ORDER
+#define SCAL_ITEM_ORDER 0
+#endif
 #ifndef SEG_UNROLL
 #define SEG_UNROLL 4
 #endif
@@ -237,8 +240,15 @@ __global__ void __launch_bounds__(128, SCAL_MINB) k_scalars(Ctx c, PanelArgs p, 
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int jt = p.jt;
   if (t >= (int64_t)jt * c.ms) return;
+#if SCAL_ITEM_ORDER == 1
+  // consecutive threads: consecutive tile rows of one shift, so a warp's
+  // segment streams are adjacent in X's column (DRAM page locality)
+  const int it = (int)(t % jt);
+  const int64_t q = t / jt;
+#else
   const int it = (int)(t / c.ms);
   const int64_t q = t % c.ms;
+#endif
   const bool cplx = q < c.mc;
   const int64_t col = cplx ? 2 * q : 2 * c.mc + (q - c.mc);
   const int64_t r0 = (int64_t)it * c.b_r;
@@ -311,7 +321,7 @@ __global__ void __launch_bounds__(128, SCAL_MINB) k_scalars(Ctx c, PanelArgs p, 
       }
     }
   }
-  RSc[t] = o;
+  RSc[(int64_t)it * c.ms + q] = o;
 }
 
 struct PanelSmem {
