@@ -46,16 +46,54 @@ def stale():
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
+def _includes(src):
+    """Headers a source includes from csrc/ (one level is enough here: the
+    .cuh files include only hsrq_device.cuh beyond what the .cu names)."""
+    deps = {src, os.path.join(ROOT, "include", "hsrq.h")}
+    todo = [src]
+    while todo:
+        f = todo.pop()
+        with open(f) as fh:
+            for line in fh:
+                line = line.strip()
+                if line.startswith("#include \"") and line.endswith(".cuh\""):
+                    d = os.path.join(CSRC, os.path.basename(line.split('"')[1]))
+                    if os.path.exists(d) and d not in deps:
+                        deps.add(d)
+                        todo.append(d)
+    return deps
+
+
 def build(force=False, verbose=False, variant=None, defines=()):
+    """One object per source (compiled in parallel, recompiled only when one of
+    its own headers changed), then one link."""
+    from concurrent.futures import ThreadPoolExecutor
+
     out = variant_lib(variant) if variant else LIB
     if not force and not variant and not stale():
         return LIB
     extra = [f"-D{d}" for d in defines]
-    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp",
-           *SOURCES]
+    objdir = os.path.join(HERE, "build", variant or "main")
+    os.makedirs(objdir, exist_ok=True)
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    jobs, objs = [], []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        fresh = (not force and os.path.exists(obj)
+                 and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in _includes(src)))
+        if not fresh:
+            jobs.append([nvcc(), *flags, *extra, "-I", os.path.join(ROOT, "include"), "-c", "-o",
+                         obj, src])
     if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+        for cmd in jobs:
+            print(" ".join(cmd))
+    with ThreadPoolExecutor(max(1, len(jobs))) as ex:
+        list(ex.map(subprocess.check_call, jobs))
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out + ".tmp", *objs]
+    if verbose:
+        print(" ".join(link))
+    subprocess.check_call(link)
     os.replace(out + ".tmp", out)
     return out
 

@@ -168,14 +168,20 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
   for (int64_t j0 = 0; j0 < n - 2; j0 += nb) {
     const int pb = (int)std::min<int64_t>(nb, n - 2 - j0);
     const int64_t L = n - j0 - 1;  // rows j0+1 .. n-1 (support of the panel's V)
+    // Rows [0, s) lie above the panel: nothing inside the panel reads them, so
+    // (as DLAHR2 / DGEHRD do) their part of Y = A V T and of the panel columns'
+    // right update is deferred to one GEMM after the panel, and the per-column
+    // level-2 product only streams rows [s, n).  s = j0 (even, so the streamed
+    // rows keep their 16-byte alignment).
+    const int64_t s = j0, Ls = n - s;
     if (!cu_ok(cudaMemsetAsync(T, 0, sizeof(double) * nb * nb, stream), "T"))
       return HSRQ_ERR_CUDA;
     for (int i = 0; i < pb; ++i) {
       const int64_t j = j0 + i;
       double* aj = A + j * lda;
       if (i > 0) {
-        // right update of column j: a_j -= Y[:, :i] V[j, :i]^T
-        dgemv(false, (int)n, i, -1.0, Y, n, V + j, n, 1.0, aj, part, stream);
+        // right update of column j, rows s..: a_j -= Y[s:, :i] V[j, :i]^T
+        dgemv(false, (int)Ls, i, -1.0, Y + s, n, V + j, n, 1.0, aj + s, part, stream);
         // left update of rows j0+1.. : a -= V T^T V^T a  (u = T^T V^T a in one launch)
         k_gemv_t_trmv<<<(unsigned)i, 256, 0, stream>>>((int)L, i, V + j0 + 1, n, aj + j0 + 1, u, T,
                                                        nb, 1, nullptr, u, counter);
@@ -185,28 +191,38 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
       k_reflector<<<1, HB_THREADS, 0, stream>>>(aj, n, j, vi, tau + i, ntau + i,
                                                  T + (size_t)i * nb + i);
       if (!cu_ok(cudaGetLastError(), "reflector")) return HSRQ_ERR_CUDA;
-      // Y[:, i] = tau (A[:, j+1:] v - Y[:, :i] (V^T v)); T[:i, i] = -tau T[:i, :i] (V^T v)
+      // Y[s:, i] = tau (A[s:, j+1:] v - Y[s:, :i] (V^T v)); T[:i, i] = -tau T[:i, :i] (V^T v)
       double* yi = Y + (size_t)i * n;
       if (i > 0)  // w = V^T v (kept raw for Y) and the T column, one launch
         k_gemv_t_trmv<<<(unsigned)i, 256, 0, stream>>>((int)L, i, V + j0 + 1, n, vi + j0 + 1, wv,
                                                        T, nb, 0, ntau + i, T + (size_t)i * nb,
                                                        counter);
-      {  // A[:, j+1:] v, reduced in chunk order with the Y correction and tau fused
+      {  // A[s:, j+1:] v, reduced in chunk order with the Y correction and tau fused
         const int nv = (int)(n - j - 1);
         const int nchunk = (nv + GV_COLS - 1) / GV_COLS;
         if (nchunk > 0)
-          k_gemv_n_part<<<dim3((unsigned)((n + GV_ROWS - 1) / GV_ROWS), (unsigned)nchunk),
-                          GV_THREADS, 0, stream>>>((int)n, nv, A + (j + 1) * lda, lda, vi + j + 1,
-                                                   1, part);
-        k_gemv_n_reduce_y<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(
-            (int)n, nchunk, part, Y, n, i, wv, tau + i, yi);
+          k_gemv_n_part<<<dim3((unsigned)((Ls + GV_ROWS - 1) / GV_ROWS), (unsigned)nchunk),
+                          GV_THREADS, 0, stream>>>((int)Ls, nv, A + (j + 1) * lda + s, lda,
+                                                   vi + j + 1, 1, part);
+        k_gemv_n_reduce_y<<<(unsigned)((Ls + 127) / 128), 128, 0, stream>>>(
+            (int)Ls, nchunk, part, Y + s, n, i, wv, tau + i, yi + s);
       }
     }
     const int64_t c0 = j0 + pb, nc = n - c0;  // trailing columns
+    if (s > 0) {
+      // the deferred rows: Y[:s] = (A[:s, j0+1:] V) T from the untouched rows, then
+      // their right update over the panel's own columns and the trailing ones
+      // (V[j, i'] = 0 for i' >= j - j0, so panel column j only sees its earlier reflectors)
+      dgemm(false, false, (int)s, pb, (int)L, 1.0, A + (j0 + 1) * lda, lda, V + j0 + 1, n, 0.0, Y,
+            n, stream);
+      k_trmm_ru<<<(unsigned)((s + 127) / 128), 128, 0, stream>>>((int)s, pb, T, nb, Y, n);
+      dgemm(false, true, (int)s, (int)L, pb, -1.0, Y, n, V + j0 + 1, n, 1.0, A + (j0 + 1) * lda,
+            lda, stream);
+    }
     if (nc > 0) {
-      // right: A[:, c0:] -= Y V[c0:, :]^T
-      dgemm(false, true, (int)n, (int)nc, pb, -1.0, Y, n, V + c0, n, 1.0, A + c0 * lda, lda,
-            stream);
+      // right: A[s:, c0:] -= Y[s:] V[c0:, :]^T
+      dgemm(false, true, (int)Ls, (int)nc, pb, -1.0, Y + s, n, V + c0, n, 1.0,
+            A + c0 * lda + s, lda, stream);
       // left: A[j0+1:, c0:] -= V T^T (V^T A[j0+1:, c0:]), with W^T = A^T V (nc x pb)
       dgemm(true, false, (int)nc, pb, (int)L, 1.0, A + c0 * lda + j0 + 1, lda, V + j0 + 1, n, 0.0,
             W, nc, stream);
