@@ -16,7 +16,8 @@
 //                    in a fixed order (deterministic); few columns: a thread
 //                    per row.
 //   k_gemv_t         y = alpha A^T x + beta y: a CTA per column.
-//   k_trmm_ru        W = W T (T upper, at most 64 x 64, in shared memory).
+//                    (W T for the panel's triangular factor is k_dgemm too: T is
+//                    kept with an explicitly zero lower triangle.)
 //   k_trmv_u         x = op(T) x for the panel's small triangular factor.
 
 namespace hblas {
@@ -171,6 +172,104 @@ __global__ void __launch_bounds__(256, 2) k_dgemm(int M, int N, int K, double al
       }
 }
 
+// C -= A B^T for K <= 64 (the blocked reduction's rank-nb updates: the right
+// and left trailing updates and the Q update), A M x K and B N x K column-
+// major.  With K this small a K-chunked pipeline is all prologue: here a CTA
+// brings its whole 128 x K and 64 x K operand panels into shared memory with
+// one burst of cp.async (two commit groups, so the MMAs start on the first K
+// half), preloads -C into the accumulators meanwhile, and runs the K loop
+// without a barrier; two CTAs per SM (100 KiB each) overlap one's loads and
+// stores with the other's DMMAs.  AL: every operand column is 16-byte aligned
+// (16-byte copies), otherwise 8-byte copies.
+constexpr int NT_K = 64;
+constexpr size_t NT_SMEM = sizeof(double) * NT_K * ((GM + 4) + (GN + 4));
+__device__ __forceinline__ void cp_async_zfill(double* dst, const double* src, int bytes, int size) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  if (size == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(bytes));
+}
+template <bool AL>
+__global__ void __launch_bounds__(256, 2) k_dgemm_nt64(int M, int N, int K, const double* A,
+                                                       int64_t lda, const double* B, int64_t ldb,
+                                                       double* C, int64_t ldc) {
+  extern __shared__ __align__(16) double nt_sm[];
+  double (*As)[GM + 4] = reinterpret_cast<double (*)[GM + 4]>(nt_sm);                 // [k][m]
+  double (*Bs)[GN + 4] = reinterpret_cast<double (*)[GN + 4]>(nt_sm + NT_K * (GM + 4));  // [k][n]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m0 = blockIdx.x * GM, n0 = blockIdx.y * GN;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int g = lane >> 2, t4 = lane & 3;
+  constexpr int W = AL ? 2 : 1;  // doubles per copy
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+#pragma unroll
+    for (int e = 0; e < (NT_K / 2) * GM / W / 256; e++) {
+      const int idx = tid + e * 256;
+      const int k = h * (NT_K / 2) + idx / (GM / W), i = (idx % (GM / W)) * W;
+      const int left = k < K ? min(W, M - (m0 + i)) : 0;
+      const double* src = left > 0 ? A + (m0 + i) + (int64_t)k * lda : A;
+      cp_async_zfill(&As[k][i], src, left > 0 ? 8 * left : 0, 8 * W);
+    }
+#pragma unroll
+    for (int e = 0; e < (NT_K / 2) * GN / W / 256; e++) {
+      const int idx = tid + e * 256;
+      const int k = h * (NT_K / 2) + idx / (GN / W), j = (idx % (GN / W)) * W;
+      const int left = k < K ? min(W, N - (n0 + j)) : 0;
+      const double* src = left > 0 ? B + (n0 + j) + (int64_t)k * ldb : B;
+      cp_async_zfill(&Bs[k][j], src, left > 0 ? 8 * left : 0, 8 * W);
+    }
+    asm volatile("cp.async.commit_group;");
+  }
+  double acc[2][4][4];
+#pragma unroll
+  for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+    for (int ni = 0; ni < 4; ni++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int r = m0 + wm * 32 + mi * 16 + g + (e >= 2 ? 8 : 0);
+        const int cc = n0 + wn * 32 + ni * 8 + 2 * t4 + (e & 1);
+        acc[mi][ni][e] = (r < M && cc < N) ? -C[r + (int64_t)cc * ldc] : 0.0;
+      }
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    if (h == 0)
+      asm volatile("cp.async.wait_group 1;");
+    else
+      asm volatile("cp.async.wait_group 0;");
+    __syncthreads();
+    if (h * (NT_K / 2) >= K) break;
+#pragma unroll
+    for (int kk = h * (NT_K / 2); kk < (h + 1) * (NT_K / 2); kk += 4) {
+      double af[2][2], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++) {
+        const int r = wm * 32 + mi * 16 + g;
+        af[mi][0] = As[kk + t4][r];
+        af[mi][1] = As[kk + t4][r + 8];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ni++) bf[ni] = Bs[kk + t4][wn * 32 + ni * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 4; ni++) mma_f64(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+    }
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+    for (int ni = 0; ni < 4; ni++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int r = m0 + wm * 32 + mi * 16 + g + (e >= 2 ? 8 : 0);
+        const int cc = n0 + wn * 32 + ni * 8 + 2 * t4 + (e & 1);
+        if (r < M && cc < N) C[r + (int64_t)cc * ldc] = -acc[mi][ni][e];
+      }
+}
+
 // y = alpha A x + beta y, A column-major m x n: partial sums of column chunks
 // of 128 into part[chunk][row], then k_gemv_n_reduce in chunk order.
 constexpr int GV_THREADS = 128, GV_ROWS = 2 * GV_THREADS, GV_COLS = 128;
@@ -263,60 +362,55 @@ __global__ void __launch_bounds__(256) k_gemv_t(int m, int n, const double* A, i
   }
 }
 
-// W = W T in place, W rows x p column-major (ldw), T p x p upper (ldt),
-// p <= 64: one thread per row, T in shared memory.
-__global__ void k_trmm_ru(int rows, int p, const double* T, int64_t ldt, double* W, int64_t ldw) {
-  __shared__ double ts[64][65];
-  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
-    const int i = e % p, j = e / p;
-    ts[i][j] = i <= j ? T[i + (int64_t)j * ldt] : 0.0;
-  }
-  __syncthreads();
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  double w[64];
-#pragma unroll 8
-  for (int i = 0; i < 64; i++) w[i] = i < p ? W[r + (int64_t)i * ldw] : 0.0;
-  for (int j = p - 1; j >= 0; j--) {  // column j uses w[0..j]
-    double s = 0.0;
-    for (int i = 0; i <= j; i++) s += w[i] * ts[i][j];
-    W[r + (int64_t)j * ldw] = s;
-  }
-}
-
 // The panel's fused column kernels (one launch where the unfused sequence
 // needed two or three; the reduction is launch-bound per column):
 //
-// k_gemv_t_trmv: y = A^T x (one CTA per column, as k_gemv_t), and the CTA
-// that finishes last (a device counter) then forms z = s op(T) y for the
-// panel's triangular factor T (p x p upper, p <= 64): trans = 1 -> z = T^T y
-// (the left update's u), trans = 0 -> z = T y (the T column); s = *scale (a
-// device scalar, e.g. -tau) or 1 when scale is NULL.  z may alias y.
+// k_gemv_t_trmv: y = A^T x (grid: columns x row ranges of rs_rows rows, the
+// partial sums of a column added in row-range order), and the CTA that
+// finishes last (a device counter) then forms z = s op(T) y for the panel's
+// triangular factor T (p x p upper, p <= 64): trans = 1 -> z = T^T y (the
+// left update's u), trans = 0 -> z = T y (the T column); s = *scale (a device
+// scalar, e.g. -tau) or 1 when scale is NULL.  z may alias y.  ypart:
+// GT_RS_MAX x 64 scratch.
+constexpr int GT_RS_MAX = 16, GT_RS_ROWS = 1024;
 __global__ void __launch_bounds__(256) k_gemv_t_trmv(int m, int n, const double* A, int64_t lda,
                                                      const double* x, double* y, const double* T,
                                                      int64_t ldt, int trans, const double* scale,
-                                                     double* z, unsigned* counter) {
+                                                     double* z, unsigned* counter, double* ypart,
+                                                     int rs_rows) {
   __shared__ double red[8];
   __shared__ bool last;
   const int col = blockIdx.x;
+  const int r0 = blockIdx.y * rs_rows, r1 = min(m, r0 + rs_rows);
   const double* a = A + (int64_t)col * lda;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < m; i += 256) s += a[i] * x[i];
+  double s0 = 0.0, s1 = 0.0;
+  int i = r0 + threadIdx.x;
+  for (; i + 256 < r1; i += 512) {
+    s0 += a[i] * x[i];
+    s1 += a[i + 256] * x[i + 256];
+  }
+  if (i < r1) s0 += a[i] * x[i];
+  double s = s0 + s1;
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < 8; w++) t += red[w];
-    y[col] = t;
+    ypart[blockIdx.y * 64 + col] = t;
     __threadfence();
-    last = atomicAdd(counter, 1u) == (unsigned)n - 1;
+    last = atomicAdd(counter, 1u) == (unsigned)n * gridDim.y - 1;
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
   __shared__ double ys[64];
-  if (threadIdx.x < n) ys[threadIdx.x] = y[threadIdx.x];
+  if (threadIdx.x < n) {
+    double t = 0.0;
+    for (unsigned rs = 0; rs < gridDim.y; rs++) t += ypart[rs * 64 + threadIdx.x];
+    ys[threadIdx.x] = t;
+    y[threadIdx.x] = t;
+  }
   __syncthreads();
   if (threadIdx.x < n) {
     const int i = threadIdx.x;
@@ -330,23 +424,38 @@ __global__ void __launch_bounds__(256) k_gemv_t_trmv(int m, int n, const double*
   }
   if (threadIdx.x == 0) *counter = 0u;  // ready for the next column
 }
+inline dim3 gemv_t_grid(int m, int n, int* rs_rows) {
+  int rs = std::min(GT_RS_MAX, std::max(1, (m + GT_RS_ROWS - 1) / GT_RS_ROWS));
+  *rs_rows = ((m + rs - 1) / rs + 1) & ~1;
+  return dim3((unsigned)n, (unsigned)((m + *rs_rows - 1) / *rs_rows));
+}
 
 // y = tau * (sum_c part[c] - Y[:, :p] w): the Av GEMV's chunk reduction fused
 // with the panel correction and the reflector's scale (DLAHR2's Y column).
-__global__ void k_gemv_n_reduce_y(int m, int nchunk, const double* part, const double* Y,
-                                  int64_t ldy, int p, const double* w, const double* tau,
-                                  double* y) {
+// Four lanes per row: lane q adds chunks / columns q, q + 4, ... in order, the
+// four sums are combined as (0 + 1) + (2 + 3).  blockDim = 128 (32 rows).
+__global__ void __launch_bounds__(128) k_gemv_n_reduce_y(int m, int nchunk, const double* part,
+                                                         const double* Y, int64_t ldy, int p,
+                                                         const double* w, const double* tau,
+                                                         double* y) {
   __shared__ double ws[64];
   if (threadIdx.x < p) ws[threadIdx.x] = w[threadIdx.x];
   __syncthreads();
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= m) return;
-  double s = 0.0;
-#pragma unroll 8
-  for (int c = 0; c < nchunk; c++) s += part[(int64_t)c * m + r];
-  double cor = 0.0;
-  for (int k = 0; k < p; k++) cor += Y[r + (int64_t)k * ldy] * ws[k];
-  y[r] = *tau * (s - cor);
+  // lanes of a quad differ in lane bits 3..4, so a warp's loads cover 8 consecutive rows
+  const int lane = threadIdx.x & 31, q = lane >> 3;
+  const int r = blockIdx.x * 32 + (threadIdx.x >> 5) * 8 + (lane & 7);
+  double s = 0.0, cor = 0.0;
+  if (r < m) {
+#pragma unroll 4
+    for (int c = q; c < nchunk; c += 4) s += part[(int64_t)c * m + r];
+#pragma unroll 4
+    for (int k = q; k < p; k += 4) cor += Y[r + (int64_t)k * ldy] * ws[k];
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 8);
+  cor += __shfl_xor_sync(0xffffffffu, cor, 8);
+  s += __shfl_xor_sync(0xffffffffu, s, 16);
+  cor += __shfl_xor_sync(0xffffffffu, cor, 16);
+  if (r < m && q == 0) y[r] = *tau * (s - cor);
 }
 
 // x = T x (trans = 0) or T^T x (trans = 1), T p x p upper (ldt), one block.
@@ -419,6 +528,26 @@ inline void dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const dou
                                                                        ldc);
     cudaFreeAsync(part, s);
   }
+}
+
+// C -= A B^T, K <= 64 (see k_dgemm_nt64)
+inline void dgemm_nt64_sub(int M, int N, int K, const double* A, int64_t lda, const double* B,
+                           int64_t ldb, double* C, int64_t ldc, cudaStream_t s) {
+  if (M <= 0 || N <= 0 || K <= 0) return;
+  const dim3 grid((unsigned)((M + GM - 1) / GM), (unsigned)((N + GN - 1) / GN));
+  const bool al = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+                    (uintptr_t)(lda * 8) | (uintptr_t)(ldb * 8)) & 15) == 0;
+  if (al)
+    k_dgemm_nt64<true><<<grid, 256, NT_SMEM, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
+  else
+    k_dgemm_nt64<false><<<grid, 256, NT_SMEM, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
+}
+inline cudaError_t dgemm_nt64_setup() {  // per call of the reduction: the attribute is per device
+  cudaError_t e = cudaFuncSetAttribute(k_dgemm_nt64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)NT_SMEM);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_dgemm_nt64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)NT_SMEM);
 }
 
 // y = alpha op(A) x + beta y; part: scratch of ceil(n / 128) * m doubles (no-trans only)

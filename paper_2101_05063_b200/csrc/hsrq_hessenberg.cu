@@ -50,21 +50,6 @@ __device__ double block_sum(double v, double* red) {
   return red[32];
 }
 
-__device__ double block_max(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-  if (w == 0)
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  __syncthreads();
-  if (threadIdx.x == 0) red[32] = v;
-  __syncthreads();
-  return red[32];
-}
-
 // Reflector of column j (testprob.py:160-172), one CTA.  a = column j of A
 // (length n, updated in place: a[j+1] = alpha, a[j+2:] = 0 unless skipped);
 // vcol = column i of V (length n: zero above row j+1); tau[i] / ntau[i] =
@@ -91,16 +76,9 @@ __global__ void __launch_bounds__(HB_THREADS) k_reflector(double* a, int64_t n, 
   const double nrm = hsrq::ghypot(x0, sqrt(tail));
   const double alpha = x0 >= 0.0 ? -nrm : nrm;
   const double v0 = x0 - alpha;
-  // ||v|| scaled (v /= np.linalg.norm(v))
-  double mx = fabs(v0);
-  for (int64_t r = 1 + threadIdx.x; r < m; r += blockDim.x) mx = fmax(mx, fabs(x[r]));
-  mx = block_max(mx, red);
-  double ss = 0.0;
-  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) {
-    const double q = (r == 0 ? v0 : x[r]) / mx;
-    ss += q * q;
-  }
-  const double vn = mx * sqrt(block_sum(ss, red));
+  // v /= np.linalg.norm(v): numpy's unscaled sqrt(v.v), and v.v = v0^2 + tail
+  // (the reference forms tail the same unscaled way, testprob.py:163)
+  const double vn = sqrt(v0 * v0 + tail);
   for (int64_t r = threadIdx.x; r < n; r += blockDim.x) {
     double v = 0.0;
     if (r > j) v = (r == j + 1 ? v0 : a[r]) / vn;
@@ -139,8 +117,8 @@ const char* hsrq_hessenberg_last_error(void) { return g_herr; }
 size_t hsrq_hessenberg_workspace_bytes(int64_t n) {
   const size_t nb = HB_NB;
   const size_t nchunk = ((size_t)n + hblas::GV_COLS - 1) / hblas::GV_COLS;
-  return sizeof(double) * ((size_t)n * nb * 2 + nb * nb + 5 * nb + nb * (size_t)n + 256 +
-                           nchunk * (size_t)n + 8);
+  return sizeof(double) * (((size_t)n + 1) * nb * 2 + nb * nb + 5 * nb + 2 * nb * ((size_t)n + 1) + 256 +
+                           nchunk * (size_t)n + hblas::GT_RS_MAX * 64 + 8);
 }
 
 int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, int64_t n,
@@ -149,16 +127,22 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
   if (ws_bytes < hsrq_hessenberg_workspace_bytes(n)) return HSRQ_ERR_WORKSPACE;
   cudaStream_t stream = (cudaStream_t)stream_;
   const int nb = HB_NB;
-  double* V = (double*)ws;              // n x nb
-  double* Y = V + (size_t)n * nb;       // n x nb
-  double* T = Y + (size_t)n * nb;       // nb x nb (upper)
+  const int64_t ne = (n + 1) & ~(int64_t)1;  // even leading dimension of V, Y, W2 (16-byte columns)
+  const int64_t ldv = ne;
+  double* V = (double*)ws;              // n x nb (ldv)
+  double* Y = V + (size_t)ldv * nb;     // n x nb (ldv)
+  double* T = Y + (size_t)ldv * nb;     // nb x nb (upper, lower triangle kept zero)
   double* tau = T + (size_t)nb * nb;    // nb
   double* ntau = tau + nb;              // nb
   double* u = ntau + nb;                // nb
   double* W = u + nb;                   // n x nb (W^T of the left update; Q V T)
   double* part = W + (size_t)nb * n + 256;  // GEMV partial sums
   double* wv = u + nb;                      // V^T v of the current column (raw), nb
-  unsigned* counter = (unsigned*)(part + ((size_t)n + hblas::GV_COLS - 1) / hblas::GV_COLS * (size_t)n);
+  double* W2 = part + ((size_t)n + hblas::GV_COLS - 1) / hblas::GV_COLS * (size_t)n;  // n x nb
+  double* ypart = W2 + (size_t)nb * (n + 1);  // GT_RS_MAX x 64
+  unsigned* counter = (unsigned*)(ypart + hblas::GT_RS_MAX * 64);
+  int rs_rows = 0;
+  if (!cu_ok(hblas::dgemm_nt64_setup(), "gemm attributes")) return HSRQ_ERR_CUDA;
   if (!cu_ok(cudaMemsetAsync(counter, 0, sizeof(unsigned), stream), "counter")) return HSRQ_ERR_CUDA;
   if (Q) {
     k_set_identity<<<(unsigned)((n * n + 255) / 256), 256, 0, stream>>>(Q, n, ldq);
@@ -181,22 +165,22 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
       double* aj = A + j * lda;
       if (i > 0) {
         // right update of column j, rows s..: a_j -= Y[s:, :i] V[j, :i]^T
-        dgemv(false, (int)Ls, i, -1.0, Y + s, n, V + j, n, 1.0, aj + s, part, stream);
+        dgemv(false, (int)Ls, i, -1.0, Y + s, ldv, V + j, ldv, 1.0, aj + s, part, stream);
         // left update of rows j0+1.. : a -= V T^T V^T a  (u = T^T V^T a in one launch)
-        k_gemv_t_trmv<<<(unsigned)i, 256, 0, stream>>>((int)L, i, V + j0 + 1, n, aj + j0 + 1, u, T,
-                                                       nb, 1, nullptr, u, counter);
-        dgemv(false, (int)L, i, -1.0, V + j0 + 1, n, u, 1, 1.0, aj + j0 + 1, part, stream);
+        k_gemv_t_trmv<<<gemv_t_grid((int)L, i, &rs_rows), 256, 0, stream>>>(
+            (int)L, i, V + j0 + 1, ldv, aj + j0 + 1, u, T, nb, 1, nullptr, u, counter, ypart, rs_rows);
+        dgemv(false, (int)L, i, -1.0, V + j0 + 1, ldv, u, 1, 1.0, aj + j0 + 1, part, stream);
       }
-      double* vi = V + (size_t)i * n;
+      double* vi = V + (size_t)i * ldv;
       k_reflector<<<1, HB_THREADS, 0, stream>>>(aj, n, j, vi, tau + i, ntau + i,
                                                  T + (size_t)i * nb + i);
       if (!cu_ok(cudaGetLastError(), "reflector")) return HSRQ_ERR_CUDA;
       // Y[s:, i] = tau (A[s:, j+1:] v - Y[s:, :i] (V^T v)); T[:i, i] = -tau T[:i, :i] (V^T v)
-      double* yi = Y + (size_t)i * n;
+      double* yi = Y + (size_t)i * ldv;
       if (i > 0)  // w = V^T v (kept raw for Y) and the T column, one launch
-        k_gemv_t_trmv<<<(unsigned)i, 256, 0, stream>>>((int)L, i, V + j0 + 1, n, vi + j0 + 1, wv,
-                                                       T, nb, 0, ntau + i, T + (size_t)i * nb,
-                                                       counter);
+        k_gemv_t_trmv<<<gemv_t_grid((int)L, i, &rs_rows), 256, 0, stream>>>(
+            (int)L, i, V + j0 + 1, ldv, vi + j0 + 1, wv, T, nb, 0, ntau + i, T + (size_t)i * nb, counter,
+            ypart, rs_rows);
       {  // A[s:, j+1:] v, reduced in chunk order with the Y correction and tau fused
         const int nv = (int)(n - j - 1);
         const int nchunk = (nv + GV_COLS - 1) / GV_COLS;
@@ -204,8 +188,8 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
           k_gemv_n_part<<<dim3((unsigned)((Ls + GV_ROWS - 1) / GV_ROWS), (unsigned)nchunk),
                           GV_THREADS, 0, stream>>>((int)Ls, nv, A + (j + 1) * lda + s, lda,
                                                    vi + j + 1, 1, part);
-        k_gemv_n_reduce_y<<<(unsigned)((Ls + 127) / 128), 128, 0, stream>>>(
-            (int)Ls, nchunk, part, Y + s, n, i, wv, tau + i, yi + s);
+        k_gemv_n_reduce_y<<<(unsigned)((Ls + 31) / 32), 128, 0, stream>>>(
+            (int)Ls, nchunk, part, Y + s, ldv, i, wv, tau + i, yi + s);
       }
     }
     const int64_t c0 = j0 + pb, nc = n - c0;  // trailing columns
@@ -213,30 +197,28 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
       // the deferred rows: Y[:s] = (A[:s, j0+1:] V) T from the untouched rows, then
       // their right update over the panel's own columns and the trailing ones
       // (V[j, i'] = 0 for i' >= j - j0, so panel column j only sees its earlier reflectors)
-      dgemm(false, false, (int)s, pb, (int)L, 1.0, A + (j0 + 1) * lda, lda, V + j0 + 1, n, 0.0, Y,
-            n, stream);
-      k_trmm_ru<<<(unsigned)((s + 127) / 128), 128, 0, stream>>>((int)s, pb, T, nb, Y, n);
-      dgemm(false, true, (int)s, (int)L, pb, -1.0, Y, n, V + j0 + 1, n, 1.0, A + (j0 + 1) * lda,
-            lda, stream);
+      dgemm(false, false, (int)s, pb, (int)L, 1.0, A + (j0 + 1) * lda, lda, V + j0 + 1, ldv, 0.0,
+            W2, ne, stream);
+      dgemm(false, false, (int)s, pb, pb, 1.0, W2, ne, T, nb, 0.0, Y, ldv, stream);  // (A V) T
+      // (columns from j0 = s: V's row j0 is zero, and the even offset keeps 16-byte copies)
+      dgemm_nt64_sub((int)s, (int)Ls, pb, Y, ldv, V + s, ldv, A + s * lda, lda, stream);
     }
     if (nc > 0) {
       // right: A[s:, c0:] -= Y[s:] V[c0:, :]^T
-      dgemm(false, true, (int)Ls, (int)nc, pb, -1.0, Y + s, n, V + c0, n, 1.0,
-            A + c0 * lda + s, lda, stream);
+      dgemm_nt64_sub((int)Ls, (int)nc, pb, Y + s, ldv, V + c0, ldv, A + c0 * lda + s, lda, stream);
       // left: A[j0+1:, c0:] -= V T^T (V^T A[j0+1:, c0:]), with W^T = A^T V (nc x pb)
-      dgemm(true, false, (int)nc, pb, (int)L, 1.0, A + c0 * lda + j0 + 1, lda, V + j0 + 1, n, 0.0,
-            W, nc, stream);
-      k_trmm_ru<<<(unsigned)((nc + 127) / 128), 128, 0, stream>>>((int)nc, pb, T, nb, W, nc);
-      dgemm(false, true, (int)L, (int)nc, pb, -1.0, V + j0 + 1, n, W, nc, 1.0,
-            A + c0 * lda + j0 + 1, lda, stream);
+      dgemm(true, false, (int)nc, pb, (int)L, 1.0, A + c0 * lda + j0 + 1, lda, V + j0 + 1, ldv,
+            0.0, W, nc, stream);
+      dgemm(false, false, (int)nc, pb, pb, 1.0, W, nc, T, nb, 0.0, W2, ne, stream);  // W T
+      // (rows from s = j0: V's row j0 is zero)
+      dgemm_nt64_sub((int)Ls, (int)nc, pb, V + s, ldv, W2, ne, A + c0 * lda + s, lda, stream);
     }
     if (Q) {
       // Q[:, j0+1:] -= (Q[:, j0+1:] V T) V^T
-      dgemm(false, false, (int)n, pb, (int)L, 1.0, Q + (j0 + 1) * ldq, ldq, V + j0 + 1, n, 0.0, W,
-            n, stream);
-      k_trmm_ru<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>((int)n, pb, T, nb, W, n);
-      dgemm(false, true, (int)n, (int)L, pb, -1.0, W, n, V + j0 + 1, n, 1.0, Q + (j0 + 1) * ldq,
-            ldq, stream);
+      dgemm(false, false, (int)n, pb, (int)L, 1.0, Q + (j0 + 1) * ldq, ldq, V + j0 + 1, ldv, 0.0,
+            W, n, stream);
+      dgemm(false, false, (int)n, pb, pb, 1.0, W, n, T, nb, 0.0, W2, ne, stream);  // (Q V) T
+      dgemm_nt64_sub((int)n, (int)Ls, pb, W2, ne, V + s, ldv, Q + s * ldq, ldq, stream);
     }
     if (!cu_ok(cudaGetLastError(), "panel kernels")) return HSRQ_ERR_CUDA;
   }
@@ -249,8 +231,14 @@ int64_t hsrq_dgemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64
                    double beta, double* C, int64_t ldc, void* stream) {
   if (M < 0 || N < 0 || K < 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
     return HSRQ_ERR_CONFIG;
-  hblas::dgemm(trans_a != 0, trans_b != 0, (int)M, (int)N, (int)K, alpha, A, lda, B, ldb, beta, C,
-               ldc, (cudaStream_t)stream);
+  if (!trans_a && trans_b && alpha == -1.0 && beta == 1.0 && K <= hblas::NT_K) {
+    // the reduction's rank-nb update shape: its own kernel (k_dgemm_nt64)
+    if (!cu_ok(hblas::dgemm_nt64_setup(), "gemm attributes")) return HSRQ_ERR_CUDA;
+    hblas::dgemm_nt64_sub((int)M, (int)N, (int)K, A, lda, B, ldb, C, ldc, (cudaStream_t)stream);
+  } else {
+    hblas::dgemm(trans_a != 0, trans_b != 0, (int)M, (int)N, (int)K, alpha, A, lda, B, ldb, beta,
+                 C, ldc, (cudaStream_t)stream);
+  }
   return cu_ok(cudaGetLastError(), "dgemm") ? 0 : HSRQ_ERR_CUDA;
 }
 

@@ -101,3 +101,45 @@ def test_front_end_dgemm_matches_fp64_reference(ta, tb, M, N, K, beta):
     torch.cuda.synchronize()
     err = (C.t() - want).abs().max().item()
     assert err <= 1e-13 * max(1.0, want.abs().max().item()) * max(1, K) ** 0.5, err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,N,K,lda,ldb,off", [
+    (257, 190, 64, 258, 190, 0),    # 16-byte copies, ragged M and N
+    (256, 128, 64, 256, 128, 0),    # exact tiles
+    (131, 67, 37, 132, 68, 0),      # partial panel (K < 64), odd extents
+    (131, 67, 37, 133, 67, 0),      # odd leading dimensions: 8-byte copies
+    (300, 200, 64, 302, 202, 1),    # operands at an odd row offset: 8-byte copies
+    (1000, 900, 5, 1000, 900, 0),   # a single K group
+])
+def test_rank_nb_update_gemm(M, N, K, lda, ldb, off):
+    """k_dgemm_nt64 (C -= A B^T, K <= 64: the blocked reduction's trailing and Q
+    updates, reached through hsrq_dgemm with alpha = -1, beta = 1) on ragged
+    shapes, both copy widths and partial panels vs a torch fp64 product;
+    elements outside the M x N block must stay untouched."""
+    import ctypes
+
+    from paper_2101_05063_b200 import _lib
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    L = _lib.load()
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn((K, lda), dtype=torch.float64, device=dev, generator=g)   # column-major M x K
+    B = torch.randn((K, ldb), dtype=torch.float64, device=dev, generator=g)   # column-major N x K
+    ldc = M + 3
+    C = torch.randn((N + 1, ldc), dtype=torch.float64, device=dev, generator=g)
+    C0 = C.clone()
+    a = A[:, off:off + M - off]
+    b = B[:, off:off + N - off]
+    m, n_ = a.shape[1], b.shape[1]
+    want = C0[:n_, :m] - b.t() @ a
+    P = lambda t, o=0: ctypes.c_void_p(t.data_ptr() + 8 * o)
+    r = L.hsrq_dgemm(0, 1, m, n_, K, -1.0, P(A, off), lda, P(B, off), ldb, 1.0, P(C), ldc,
+                     ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert r == 0
+    torch.cuda.synchronize()
+    err = (C[:n_, :m] - want).abs().max().item()
+    assert err <= 1e-13 * max(1.0, want.abs().max().item()) * K ** 0.5, err
+    assert torch.equal(C[:n_, m:], C0[:n_, m:]) and torch.equal(C[n_:], C0[n_:])
