@@ -116,8 +116,10 @@ struct Ctx {
   double* HM0;           // N x N : max |H[tile i rows, js-1]|
   double* RS;            // N x N : max row sum |H[tile i rows, js:je-1]|
   double* HMK;           // N x MAXK : max_{i<kp} |h(i, kp-1)| of each diagonal tile
-  double* XB;            // N x ms: max |X| over each tile's rows (real: exact;
-                         // complex: max(|re|+|im|), an upper bound of max |x|)
+  double* XB;            // 2 x N x ms: max |X| over each tile's rows (real: exact;
+                         // complex: max(|re|+|im|), an upper bound of max |x|) =
+                         // the larger of the two halves (k_panel_cl: one per CTA
+                         // of the pair; every other writer: [0] = max, [1] = 0)
   int64_t* fail;         // ms
   unsigned long long* nfail;
   int robust, mode;
@@ -257,6 +259,7 @@ __global__ void k_zero_state(Ctx c, int zero_tables) {
   if (t < ne) {
     c.E[t] = 0;
     c.XB[t] = 0.0;
+    c.XB[ne + t] = 0.0;
   }
   if (t < c.ms) c.fail[t] = 0;
   if (zero_tables && t < (int64_t)c.N * c.N) {
@@ -672,8 +675,8 @@ WsLayout ws_layout(int64_t n, int b_r, int64_t mc, int64_t mr) {
   off = align_up(off + sizeof(double) * (size_t)N * N, 256);
   L.hmk = off;
   off = align_up(off + sizeof(double) * (size_t)N * MAXK, 256);
-  L.xb = off;
-  off = align_up(off + sizeof(double) * (size_t)N * ms, 256);
+  L.xb = off;  // two halves (the cluster panel writes one per CTA of a pair)
+  off = align_up(off + 2 * sizeof(double) * (size_t)N * ms, 256);
   L.rsc = off;
   off = align_up(off + 64 * (size_t)N * ms, 256);
   L.rt = off;

@@ -256,7 +256,8 @@ __global__ void __launch_bounds__(128, SCAL_MINB) k_scalars(Ctx c, PanelArgs p, 
   const double* Xi = Xr + c.ldx;
   RowScalars o;
   HSRQ_COUNT(8);
-  double bmax = c.XB[(int64_t)it * c.ms + q];  // real: exact max|b|; complex: bound
+  // real: exact max|b|; complex: bound (two halves, see Ctx::XB)
+  double bmax = fmax(c.XB[(int64_t)it * c.ms + q], c.XB[((int64_t)c.N + it) * c.ms + q]);
   if (!scalars_step1(c, jt, it, q, bmax, !cplx, o)) {
     HSRQ_COUNT(9);
     // near overflow: max|b| from scaled squared moduli (an interval of
@@ -721,11 +722,13 @@ __device__ __forceinline__ void epilogue_b128(const Ctx& c, const PanelArgs& p, 
     if (v0) {
       if (robust) c.E[ix0] = sm.dex[0][cl0];
       c.XB[ix0] = mb0;
+      c.XB[(int64_t)c.N * c.ms + ix0] = 0.0;
     }
     if (v1 && !cplx) {
       const int64_t ix1 = (int64_t)tile0 * c.ms + q1;
       if (robust) c.E[ix1] = sm.dex[0][cl0 + 1];
       c.XB[ix1] = mb1;
+      c.XB[(int64_t)c.N * c.ms + ix1] = 0.0;
     }
   }
   tl_mark(tlp, 4);
@@ -1138,6 +1141,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) k_panel(Ctx c, PanelArgs p,
     const int64_t ix = (int64_t)(tile0 + sg) * c.ms + q;
     if (robust) c.E[ix] = sm.dex[sg][cc];
     c.XB[ix] = dval(sm.red[0][sg][cc]);
+    c.XB[(int64_t)c.N * c.ms + ix] = 0.0;
   }
   if (tl_) {
     unsigned long long g;

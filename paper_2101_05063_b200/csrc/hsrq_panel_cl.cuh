@@ -9,9 +9,13 @@
 // epilogue three keep the DMMA pipe fed (two 8-warp CTAs: the lone GEMM CTA
 // reached 71 % of the pair's rate, which exposed ~90 ms of epilogue per
 // config-5 solve).  Step 3's guard needs maxima over the whole tile row:
-// each CTA reduces its 64 rows, the pair exchanges them through distributed
-// shared memory (one cluster barrier), and both evaluate the identical guard
-// -- the rare exact-moduli path and the next column's XB bound likewise.
+// each CTA reduces its 64 rows and PUSHES them into its peer's shared memory
+// (distributed shared memory stores, one cluster barrier), and both evaluate
+// the identical guard from local memory -- the rare exact-moduli path
+// likewise.  Nothing reads remote memory after a barrier, so a CTA may exit
+// while its peer still works: no trailing cluster barriers.  The next
+// column's XB bound is written per half (c.XB / c.XB + N ms), its reader
+// (k_scalars) takes the larger.
 
 #undef HSRQ_FUZZ_FILE
 #define HSRQ_FUZZ_FILE 4u
@@ -23,6 +27,10 @@ constexpr int CL_THREADS = 128;           // 4 warps: 2 (M) x 2 (N) warp tiles o
 constexpr int CL_STAGES = 2;
 constexpr int CL_ROWS = 8;                // epilogue: threads per column pair
 constexpr int CL_RPT = CL_BM / CL_ROWS;   // rows per thread (8)
+// C row stride: the epilogue's four column pairs per warp read rows 4 apart;
+// 4 * 66 doubles = 16 banks mod 32, so they pair up on the two 128-byte
+// wavefronts a 64-bit warp read needs anyway (stride 68: all four collide)
+constexpr int CL_CPAD = CL_BM + 2;
 #ifndef CL_MINB
 #define CL_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
@@ -33,12 +41,13 @@ struct PanelClSmem {
       double A[CL_STAGES][BK][CL_BM + 4];
       double B[CL_STAGES][2 * BN][BPAD];
     } pipe;
-    double C[2 * BN][CL_BM + 4];  // accumulators, [acc col][row]
+    double C[2 * BN][CL_CPAD];  // accumulators, [acc col][row]
   } u;
   RowScalars rsc[BN];
-  unsigned long long red[2][BN];   // pass-1 maxima of this CTA's rows (read by the peer)
-  unsigned long long hred[2][BN];  // exact glibc-moduli maxima (rare path, read by the peer)
-  double xbm[BN];                  // pass-2 maxima (the next column's XB, read by rank 0)
+  unsigned long long red[2][BN];    // pass-1 maxima of this CTA's rows
+  unsigned long long redp[2][BN];   // ... of the peer's rows (written by the peer)
+  unsigned long long hred[2][BN];   // exact glibc-moduli maxima (rare path)
+  unsigned long long hredp[2][BN];  // ... of the peer's rows (written by the peer)
   double x3[BN], z3r[BN], z3i[BN];
   int dex[BN];
   int need[BN];
@@ -92,7 +101,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CL_THREADS, CL_MINB)
       const int64_t q = col < 2 * c.mc ? col / 2 : c.mc + (col - 2 * c.mc);
       sm.rsc[cc] = RSc[(int64_t)tile0 * c.ms + q];
     }
-    sm.red[0][cc] = sm.red[1][cc] = 0ULL;
     sm.need[cc] = 0;
   }
 
@@ -239,12 +247,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CL_THREADS, CL_MINB)
     mr1 = fmax(mr1, __shfl_xor_sync(0xffffffffu, mr1, o));
   }
   if (rp == 0) {
-    sm.red[0][cl0] = dkey(mb0);
-    sm.red[0][cl0 + 1] = dkey(mb1);
-    sm.red[1][cl0] = dkey(mr0);
-    sm.red[1][cl0 + 1] = dkey(mr1);
+    sm.red[0][cl0] = peer.redp[0][cl0] = dkey(mb0);
+    sm.red[0][cl0 + 1] = peer.redp[0][cl0 + 1] = dkey(mb1);
+    sm.red[1][cl0] = peer.redp[1][cl0] = dkey(mr0);
+    sm.red[1][cl0 + 1] = peer.redp[1][cl0 + 1] = dkey(mr1);
   }
-  cluster.sync();  // both halves' maxima visible (distributed shared memory)
+  cluster.sync();  // both halves' maxima in both CTAs (pushed through distributed shared memory)
   // ---- step 3 guard (:287-301), one thread per column, on the tile row's maxima ----
   int my_need = 0;
   if (tid < BN) {
@@ -255,8 +263,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CL_THREADS, CL_MINB)
       double zr = s.zkr, zi = s.zki, x3 = 1.0;
       int dx = s.dexp;
       if (robust) {
-        const unsigned long long kb = sm.red[0][cc] > peer.red[0][cc] ? sm.red[0][cc] : peer.red[0][cc];
-        const unsigned long long kr = sm.red[1][cc] > peer.red[1][cc] ? sm.red[1][cc] : peer.red[1][cc];
+        const unsigned long long kb = sm.red[0][cc] > sm.redp[0][cc] ? sm.red[0][cc] : sm.redp[0][cc];
+        const unsigned long long kr = sm.red[1][cc] > sm.redp[1][cc] ? sm.red[1][cc] : sm.redp[1][cc];
         const double bb = dval(kb), rb = dval(kr);
         if (col < 2 * c.mc) {
           if (!protect_update_is_one(bb * BOUND_SLACK, rb * BOUND_SLACK,
@@ -295,14 +303,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CL_THREADS, CL_MINB)
       hr = fmax(hr, __shfl_xor_sync(0xffffffffu, hr, o));
     }
     if (rp == 0 && cplx) {
-      sm.hred[0][cl0] = dkey(hb);
-      sm.hred[1][cl0] = dkey(hr);
+      sm.hred[0][cl0] = peer.hredp[0][cl0] = dkey(hb);
+      sm.hred[1][cl0] = peer.hredp[1][cl0] = dkey(hr);
     }
     cluster.sync();
     if (tid < BN && sm.need[tid]) {
       const int cc = tid, ccr = cc & ~1;
-      const unsigned long long kb = sm.hred[0][ccr] > peer.hred[0][ccr] ? sm.hred[0][ccr] : peer.hred[0][ccr];
-      const unsigned long long kr = sm.hred[1][ccr] > peer.hred[1][ccr] ? sm.hred[1][ccr] : peer.hred[1][ccr];
+      const unsigned long long kb = sm.hred[0][ccr] > sm.hredp[0][ccr] ? sm.hred[0][ccr] : sm.hredp[0][ccr];
+      const unsigned long long kr = sm.hred[1][ccr] > sm.hredp[1][ccr] ? sm.hred[1][ccr] : sm.hredp[1][ccr];
       const double zr = sm.z3r[cc], zi = sm.z3i[cc];
       const int xe = protect_update_e(dval(kb), dval(kr), ghypot(zr, zi), c.omega);
       if (xe < 0) {
@@ -383,23 +391,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CL_THREADS, CL_MINB)
     mb0 = fmax(mb0, __shfl_xor_sync(0xffffffffu, mb0, o));
     mb1 = fmax(mb1, __shfl_xor_sync(0xffffffffu, mb1, o));
   }
+  // new beta (rank 0) and this half's share of the step-1 bound for the next tile column
   if (rp == 0) {
-    sm.xbm[cl0] = mb0;
-    sm.xbm[cl0 + 1] = mb1;
-  }
-  cluster.sync();
-  // new beta and the step-1 bound for the next tile column (rank 0, one lane per column)
-  if (rank == 0 && rp == 0) {
+    const int64_t half = (int64_t)rank * c.N * c.ms;
     const int64_t ix0 = (int64_t)tile0 * c.ms + q0;
     if (v0) {
-      if (robust) c.E[ix0] = sm.dex[cl0];
-      c.XB[ix0] = fmax(mb0, peer.xbm[cl0]);
+      if (robust && rank == 0) c.E[ix0] = sm.dex[cl0];
+      c.XB[half + ix0] = mb0;
     }
     if (v1 && !cplx) {
       const int64_t ix1 = (int64_t)tile0 * c.ms + q1;
-      if (robust) c.E[ix1] = sm.dex[cl0 + 1];
-      c.XB[ix1] = fmax(mb1, peer.xbm[cl0 + 1]);
+      if (robust && rank == 0) c.E[ix1] = sm.dex[cl0 + 1];
+      c.XB[half + ix1] = mb1;
     }
   }
-  cluster.sync();  // rank 1's shared memory stays alive until rank 0 has read it
 }

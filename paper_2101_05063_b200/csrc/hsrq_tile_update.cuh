@@ -77,6 +77,7 @@ __global__ void k_tile_xb(Ctx c) {
     if (v > mx) mx = v;
   }
   c.XB[t] = mx;
+  c.XB[(int64_t)c.N * c.ms + t] = 0.0;
 }
 
 // The diagonal sweep's operand code on the caller's x_below and rotations:
