@@ -534,7 +534,7 @@ def run_gpu(args):
 
     peak, peak_src, hbm = load_peaks()
     traffic, traffic_note = None, None
-    prof_rel = "profiles/ncu_r02_k_panel_cl_cfg5_jt84.json"
+    prof_rel = "profiles/ncu_r02c_k_panel_cl_cfg5_jt84.json"
     prof = os.path.join(ROOT, prof_rel)
     if os.path.exists(prof) and n == 16000:
         with open(prof) as f:
