@@ -172,6 +172,138 @@ __global__ void __launch_bounds__(256, 2) k_dgemm(int M, int N, int K, double al
       }
 }
 
+// 16-byte (or zero-filled shorter) asynchronous copy global -> shared
+__device__ __forceinline__ void cp_async16_zfill(double* dst, const double* src, int bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes));
+}
+
+// k_dgemm with the operands staged by a three-stage cp.async pipeline (the
+// register-prefetch kernel above exposes one global-load latency per K chunk
+// behind two barriers).  Needs 16-byte aligned operand columns (even leading
+// dimensions, aligned bases); dgemm() falls back to k_dgemm otherwise.  Each
+// operand lands in shared memory in the orientation its memory layout allows
+// 16-byte copies for: A [k][m] (not transposed) or [m][k] (transposed),
+// B [n][k] (not transposed) or [k][n] (transposed); the row strides (+4) keep
+// the fragment reads conflict-free either way.
+constexpr int GP_STAGES = 3;
+constexpr int GP_A = GM * (GK + 4), GP_B = GN * (GK + 4);  // doubles per stage (the larger orientation)
+constexpr size_t GP_SMEM = sizeof(double) * GP_STAGES * (GP_A + GP_B);
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256, 2) k_dgemm_pipe(int M, int N, int K, double alpha,
+                                                       const double* A, int64_t lda,
+                                                       const double* B, int64_t ldb, double beta,
+                                                       double* C, int64_t ldc, int kchunk,
+                                                       double* part) {
+  extern __shared__ __align__(16) double gp_sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m0 = blockIdx.x * GM, n0 = blockIdx.y * GN;
+  const int kz0 = blockIdx.z * kchunk, kz1 = min(K, kz0 + kchunk);
+  const int nk = (kz1 - kz0 + GK - 1) / GK;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int g = lane >> 2, t4 = lane & 3;
+  constexpr int LDA_S = TA ? GK + 4 : GM + 4;  // As[m][k] : As[k][m]
+  constexpr int LDB_S = TB ? GN + 4 : GK + 4;  // Bs[k][n] : Bs[n][k]
+  auto As = [&](int st) { return gp_sm + st * (GP_A + GP_B); };
+  auto Bs = [&](int st) { return gp_sm + st * (GP_A + GP_B) + GP_A; };
+  auto load = [&](int st, int kc) {
+    const int k0 = kz0 + kc * GK;
+    double* as = As(st);
+    double* bs = Bs(st);
+#pragma unroll
+    for (int e = 0; e < GM * GK / 2 / 256; e++) {
+      const int idx = tid + e * 256;
+      if (TA) {  // pairs along k at one row i of op(A)
+        const int i = idx / (GK / 2), k = (idx % (GK / 2)) * 2;
+        const int left = (m0 + i < M) ? min(2, kz1 - (k0 + k)) : 0;
+        const double* src = left > 0 ? A + (k0 + k) + (int64_t)(m0 + i) * lda : A;
+        cp_async16_zfill(as + i * LDA_S + k, src, left > 0 ? 8 * left : 0);
+      } else {   // pairs along m at one k
+        const int k = idx / (GM / 2), i = (idx % (GM / 2)) * 2;
+        const int left = (k0 + k < kz1) ? min(2, M - (m0 + i)) : 0;
+        const double* src = left > 0 ? A + (m0 + i) + (int64_t)(k0 + k) * lda : A;
+        cp_async16_zfill(as + k * LDA_S + i, src, left > 0 ? 8 * left : 0);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < GN * GK / 2 / 256; e++) {
+      const int idx = tid + e * 256;
+      if (TB) {  // op(B)[k][j] = B[j + k ldb]: pairs along n at one k
+        const int k = idx / (GN / 2), j = (idx % (GN / 2)) * 2;
+        const int left = (k0 + k < kz1) ? min(2, N - (n0 + j)) : 0;
+        const double* src = left > 0 ? B + (n0 + j) + (int64_t)(k0 + k) * ldb : B;
+        cp_async16_zfill(bs + k * LDB_S + j, src, left > 0 ? 8 * left : 0);
+      } else {   // op(B)[k][j] = B[k + j ldb]: pairs along k at one column j
+        const int j = idx / (GK / 2), k = (idx % (GK / 2)) * 2;
+        const int left = (n0 + j < N) ? min(2, kz1 - (k0 + k)) : 0;
+        const double* src = left > 0 ? B + (k0 + k) + (int64_t)(n0 + j) * ldb : B;
+        cp_async16_zfill(bs + j * LDB_S + k, src, left > 0 ? 8 * left : 0);
+      }
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < GP_STAGES - 1; st++) {
+    if (st < nk) load(st, st);
+    asm volatile("cp.async.commit_group;");
+  }
+  double acc[2][4][4];
+  const bool pre = part == nullptr && beta != 0.0;
+  const double ba = pre ? beta / alpha : 0.0;
+#pragma unroll
+  for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+    for (int ni = 0; ni < 4; ni++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int r = m0 + wm * 32 + mi * 16 + g + (e >= 2 ? 8 : 0);
+        const int cc = n0 + wn * 32 + ni * 8 + 2 * t4 + (e & 1);
+        acc[mi][ni][e] = (pre && r < M && cc < N) ? ba * C[r + (int64_t)cc * ldc] : 0.0;
+      }
+  for (int kc = 0; kc < nk; kc++) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(GP_STAGES - 2));
+    __syncthreads();
+    if (kc + GP_STAGES - 1 < nk) load((kc + GP_STAGES - 1) % GP_STAGES, kc + GP_STAGES - 1);
+    asm volatile("cp.async.commit_group;");
+    const double* as = As(kc % GP_STAGES);
+    const double* bs = Bs(kc % GP_STAGES);
+#pragma unroll
+    for (int kk = 0; kk < GK; kk += 4) {
+      double af[2][2], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++) {
+        const int r = wm * 32 + mi * 16 + g;
+        af[mi][0] = TA ? as[r * LDA_S + kk + t4] : as[(kk + t4) * LDA_S + r];
+        af[mi][1] = TA ? as[(r + 8) * LDA_S + kk + t4] : as[(kk + t4) * LDA_S + r + 8];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ni++) {
+        const int cn = wn * 32 + ni * 8 + g;
+        bf[ni] = TB ? bs[(kk + t4) * LDB_S + cn] : bs[cn * LDB_S + kk + t4];
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 4; ni++) mma_f64(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;");
+#pragma unroll
+  for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+    for (int ni = 0; ni < 4; ni++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int r = m0 + wm * 32 + mi * 16 + g + (e >= 2 ? 8 : 0);
+        const int cc = n0 + wn * 32 + ni * 8 + 2 * t4 + (e & 1);
+        if (r < M && cc < N) {
+          if (part)
+            part[((int64_t)blockIdx.z * N + cc) * M + r] = acc[mi][ni][e];
+          else
+            C[r + (int64_t)cc * ldc] = alpha * acc[mi][ni][e];
+        }
+      }
+}
+
 // C -= A B^T for K <= 64 (the blocked reduction's rank-nb updates: the right
 // and left trailing updates and the Q update), A M x K and B N x K column-
 // major.  With K this small a K-chunked pipeline is all prologue: here a CTA
@@ -495,6 +627,19 @@ __global__ void k_dgemm_splitk_reduce(int M, int N, int S, const double* part, d
 
 // ---- host wrappers (stream-ordered, column-major, cuBLAS argument order) ----
 
+// The pipelined kernels need their dynamic shared-memory limit raised on the
+// current device; entry points call dgemm_pipe_setup() first (cheap, idempotent).
+static thread_local bool g_pipe_ready = false;
+inline cudaError_t dgemm_pipe_setup() {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_dgemm_pipe<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_dgemm_pipe<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_dgemm_pipe<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_dgemm_pipe<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GP_SMEM)) != cudaSuccess) return e;
+  g_pipe_ready = true;
+  return cudaSuccess;
+}
+
 inline void dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
                   int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                   cudaStream_t s) {
@@ -514,7 +659,19 @@ inline void dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const dou
   }
   const dim3 grid(grid2.x, grid2.y, (unsigned)S);
   const int kc = S > 1 ? kchunk : K;
-  if (!ta && !tb)
+  // 16-byte aligned operand columns: the cp.async pipeline (dgemm_pipe_setup() once per device)
+  const bool al = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+                    (uintptr_t)(lda * 8) | (uintptr_t)(ldb * 8)) & 15) == 0;
+  if (al && g_pipe_ready) {
+    if (!ta && !tb)
+      k_dgemm_pipe<false, false><<<grid, 256, GP_SMEM, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, part);
+    else if (!ta && tb)
+      k_dgemm_pipe<false, true><<<grid, 256, GP_SMEM, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, part);
+    else if (ta && !tb)
+      k_dgemm_pipe<true, false><<<grid, 256, GP_SMEM, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, part);
+    else
+      k_dgemm_pipe<true, true><<<grid, 256, GP_SMEM, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, part);
+  } else if (!ta && !tb)
     k_dgemm<false, false><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, part);
   else if (!ta && tb)
     k_dgemm<false, true><<<grid, 256, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, part);

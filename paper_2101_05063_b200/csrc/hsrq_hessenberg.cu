@@ -118,7 +118,7 @@ size_t hsrq_hessenberg_workspace_bytes(int64_t n) {
   const size_t nb = HB_NB;
   const size_t nchunk = ((size_t)n + hblas::GV_COLS - 1) / hblas::GV_COLS;
   return sizeof(double) * (((size_t)n + 1) * nb * 2 + nb * nb + 5 * nb + 2 * nb * ((size_t)n + 1) + 256 +
-                           nchunk * (size_t)n + hblas::GT_RS_MAX * 64 + 8);
+                           nchunk * (size_t)n + 1 + hblas::GT_RS_MAX * 64 + 8);
 }
 
 int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, int64_t n,
@@ -138,11 +138,13 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
   double* W = u + nb;                   // n x nb (W^T of the left update; Q V T)
   double* part = W + (size_t)nb * n + 256;  // GEMV partial sums
   double* wv = u + nb;                      // V^T v of the current column (raw), nb
-  double* W2 = part + ((size_t)n + hblas::GV_COLS - 1) / hblas::GV_COLS * (size_t)n;  // n x nb
+  // n x nb (ne); the partial-sum block is rounded up to an even count to keep W2 16-byte aligned
+  double* W2 = part + ((((size_t)n + hblas::GV_COLS - 1) / hblas::GV_COLS * (size_t)n + 1) & ~(size_t)1);
   double* ypart = W2 + (size_t)nb * (n + 1);  // GT_RS_MAX x 64
   unsigned* counter = (unsigned*)(ypart + hblas::GT_RS_MAX * 64);
   int rs_rows = 0;
   if (!cu_ok(hblas::dgemm_nt64_setup(), "gemm attributes")) return HSRQ_ERR_CUDA;
+  if (!cu_ok(hblas::dgemm_pipe_setup(), "gemm attributes")) return HSRQ_ERR_CUDA;
   if (!cu_ok(cudaMemsetAsync(counter, 0, sizeof(unsigned), stream), "counter")) return HSRQ_ERR_CUDA;
   if (Q) {
     k_set_identity<<<(unsigned)((n * n + 255) / 256), 256, 0, stream>>>(Q, n, ldq);
@@ -197,8 +199,10 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
       // the deferred rows: Y[:s] = (A[:s, j0+1:] V) T from the untouched rows, then
       // their right update over the panel's own columns and the trailing ones
       // (V[j, i'] = 0 for i' >= j - j0, so panel column j only sees its earlier reflectors)
-      dgemm(false, false, (int)s, pb, (int)L, 1.0, A + (j0 + 1) * lda, lda, V + j0 + 1, ldv, 0.0,
-            W2, ne, stream);
+      // (K from row / column j0: V's row j0 is zero, and the even offset keeps the
+      // operands 16-byte aligned for the pipelined GEMM)
+      dgemm(false, false, (int)s, pb, (int)Ls, 1.0, A + s * lda, lda, V + s, ldv, 0.0, W2, ne,
+            stream);
       dgemm(false, false, (int)s, pb, pb, 1.0, W2, ne, T, nb, 0.0, Y, ldv, stream);  // (A V) T
       // (columns from j0 = s: V's row j0 is zero, and the even offset keeps 16-byte copies)
       dgemm_nt64_sub((int)s, (int)Ls, pb, Y, ldv, V + s, ldv, A + s * lda, lda, stream);
@@ -207,17 +211,17 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
       // right: A[s:, c0:] -= Y[s:] V[c0:, :]^T
       dgemm_nt64_sub((int)Ls, (int)nc, pb, Y + s, ldv, V + c0, ldv, A + c0 * lda + s, lda, stream);
       // left: A[j0+1:, c0:] -= V T^T (V^T A[j0+1:, c0:]), with W^T = A^T V (nc x pb)
-      dgemm(true, false, (int)nc, pb, (int)L, 1.0, A + c0 * lda + j0 + 1, lda, V + j0 + 1, ldv,
-            0.0, W, nc, stream);
-      dgemm(false, false, (int)nc, pb, pb, 1.0, W, nc, T, nb, 0.0, W2, ne, stream);  // W T
+      dgemm(true, false, (int)nc, pb, (int)Ls, 1.0, A + c0 * lda + s, lda, V + s, ldv, 0.0, W, ne,
+            stream);
+      dgemm(false, false, (int)nc, pb, pb, 1.0, W, ne, T, nb, 0.0, W2, ne, stream);  // W T
       // (rows from s = j0: V's row j0 is zero)
       dgemm_nt64_sub((int)Ls, (int)nc, pb, V + s, ldv, W2, ne, A + c0 * lda + s, lda, stream);
     }
     if (Q) {
       // Q[:, j0+1:] -= (Q[:, j0+1:] V T) V^T
-      dgemm(false, false, (int)n, pb, (int)L, 1.0, Q + (j0 + 1) * ldq, ldq, V + j0 + 1, ldv, 0.0,
-            W, n, stream);
-      dgemm(false, false, (int)n, pb, pb, 1.0, W, n, T, nb, 0.0, W2, ne, stream);  // (Q V) T
+      dgemm(false, false, (int)n, pb, (int)Ls, 1.0, Q + s * ldq, ldq, V + s, ldv, 0.0, W, ne,
+            stream);
+      dgemm(false, false, (int)n, pb, pb, 1.0, W, ne, T, nb, 0.0, W2, ne, stream);  // (Q V) T
       dgemm_nt64_sub((int)n, (int)Ls, pb, W2, ne, V + s, ldv, Q + s * ldq, ldq, stream);
     }
     if (!cu_ok(cudaGetLastError(), "panel kernels")) return HSRQ_ERR_CUDA;
@@ -236,6 +240,7 @@ int64_t hsrq_dgemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64
     if (!cu_ok(hblas::dgemm_nt64_setup(), "gemm attributes")) return HSRQ_ERR_CUDA;
     hblas::dgemm_nt64_sub((int)M, (int)N, (int)K, A, lda, B, ldb, C, ldc, (cudaStream_t)stream);
   } else {
+    if (!cu_ok(hblas::dgemm_pipe_setup(), "gemm attributes")) return HSRQ_ERR_CUDA;
     hblas::dgemm(trans_a != 0, trans_b != 0, (int)M, (int)N, (int)K, alpha, A, lda, B, ldb, beta,
                  C, ldc, (cudaStream_t)stream);
   }
@@ -246,6 +251,7 @@ int64_t hsrq_backmultiply(const double* Q, int64_t ldq, int64_t n, const double*
                           int64_t ncol, double* Z, int64_t ldz, void* stream_) {
   if (n < 1 || ncol < 0 || ldq < n || ldx < n || ldz < n) return HSRQ_ERR_CONFIG;
   if (ncol == 0) return 0;
+  if (!cu_ok(hblas::dgemm_pipe_setup(), "gemm attributes")) return HSRQ_ERR_CUDA;
   hblas::dgemm(false, false, (int)n, (int)ncol, (int)n, 1.0, Q, ldq, X, ldx, 0.0, Z, ldz,
                (cudaStream_t)stream_);
   return cu_ok(cudaGetLastError(), "gemm qx") ? 0 : HSRQ_ERR_CUDA;

@@ -73,7 +73,11 @@ def test_backmultiply_and_dense_pipeline():
 
 @pytest.mark.parametrize("ta,tb,M,N,K,beta", [
     (0, 0, 300, 70, 129, 0.0), (0, 1, 257, 190, 64, 1.0), (1, 0, 1000, 64, 3000, 0.0),
-    (1, 1, 33, 17, 5, 0.5), (0, 0, 500, 64, 5000, 0.25), (0, 1, 128, 64, 16, -1.0)])
+    (1, 1, 33, 17, 5, 0.5), (0, 0, 500, 64, 5000, 0.25), (0, 1, 128, 64, 16, -1.0),
+    # even leading dimensions: the cp.async-pipelined kernel, ragged tiles and K tails
+    (0, 0, 300, 70, 130, 0.0), (0, 1, 258, 190, 66, 1.0), (1, 0, 1000, 64, 3002, 0.0),
+    (1, 1, 34, 18, 6, 0.5), (0, 0, 130, 2, 2, 0.0), (1, 0, 64, 200, 17 * 2, -0.5),
+    (0, 1, 2, 2, 1000, 2.0)])
 def test_front_end_dgemm_matches_fp64_reference(ta, tb, M, N, K, beta):
     """hsrq_dgemm (the front end's DMMA GEMM, csrc/hsrq_blas.cuh) on ragged
     shapes, every transpose combination, beta != 0 (accumulator preload) and
