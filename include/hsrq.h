@@ -346,7 +346,10 @@ int64_t hsrq_backmultiply(const double* Q, int64_t ldq, int64_t n, const double*
                           int64_t ncol, double* Z, int64_t ldz, void* stream);
 const char* hsrq_hessenberg_last_error(void);
 /* The front end's fp64 GEMM (csrc/hsrq_blas.cuh, DMMA), exposed for tests:
- * C = alpha op(A) op(B) + beta C, column-major, op = transpose if trans_*. */
+ * C = alpha op(A) op(B) + beta C, column-major, op = transpose if trans_*.
+ * Dispatch: the rank-nb update shape (A B^T, alpha = -1, beta = 1, K <= 64)
+ * runs k_dgemm_nt64; operands with 16-byte aligned columns the cp.async
+ * pipeline k_dgemm_pipe; anything else the register-prefetch k_dgemm. */
 int64_t hsrq_dgemm(int32_t trans_a, int32_t trans_b, int64_t M, int64_t N, int64_t K,
                    double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                    double beta, double* C, int64_t ldc, void* stream);
