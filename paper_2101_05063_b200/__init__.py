@@ -16,6 +16,8 @@ from .core import (
     SingularSystemError,
     SolutionBlock,
     StructuralViolationError,
+    TaskError,
+    TaskNode,
     TileGrid,
 )
 from .inviter import (

@@ -64,7 +64,7 @@ def _driver(h, shifts, b, kind, *, b_r=None, b_c=32, workers=1, robust=True, mod
         workspace.peak_crossover_reals = max(workspace.peak_crossover_reals,
                                              n * N * m * (2 if cplx else 1))
     if out.nfail:
-        raise_first_failure(out.fail.cpu().numpy(), b_c, [(0, m)])
+        raise_first_failure(out.fail.cpu().numpy(), b_c, [(0, m)], n_tiles=(n + b_r - 1) // b_r)
     return to_solution_block(out, n, robust=robust, want_cplx=cplx)
 
 

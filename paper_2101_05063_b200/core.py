@@ -35,6 +35,74 @@ class StructuralViolationError(HessrqError):
     """Input violates the unreduced-Hessenberg structure (core.py:56-57)."""
 
 
+@dataclass
+class TaskNode:
+    """The reference's task-graph node (scheduler.py:35-43) as far as a failure
+    report needs it: ``kind`` ("ReduceDiag", "SolveTile",
+    "MergedSolveBacktransform"), ``coords`` = (tile_i, tile_j, batch) and the
+    node's position ``seq`` in the reference's graph (scheduler.py:120-179)."""
+
+    kind: str
+    coords: tuple
+    seq: int = None
+    run: object = None
+
+    def __repr__(self):
+        return f"TaskNode({self.kind}, coords={self.coords})"
+
+
+class TaskError(Exception):
+    """What a caller of the reference actually catches when a kernel fails: the
+    executor aborts the graph and re-raises the kernel's error wrapped with the
+    failing node (scheduler.py:182-187, 211-214) -- ``node``, ``cause``, the
+    message ``task <kind> at <coords> failed: <cause>``, ``__cause__`` set."""
+
+    def __init__(self, node, cause):
+        Exception.__init__(self, f"task {node.kind} at {node.coords} failed: {cause}")
+        self.node = node
+        self.cause = cause
+
+
+class SingularTaskError(TaskError, SingularSystemError):
+    """The TaskError of a singular pivot.  It is also a SingularSystemError
+    (``shift_index`` / ``local_index`` of the cause), so both ``except
+    TaskError`` written against the reference's drivers and ``except
+    SingularSystemError`` written against its kernels' error type catch it."""
+
+    def __init__(self, node, cause):
+        TaskError.__init__(self, node, cause)
+        self.shift_index = cause.shift_index
+        self.local_index = cause.local_index
+
+
+class StructuralTaskError(TaskError, StructuralViolationError):
+    """The TaskError of a degenerate rotation; also a StructuralViolationError."""
+
+
+def task_node_of_failure(phase_singular, tile, batch, n_tiles):
+    """The reference graph node in which a kernel failure surfaces: a degenerate
+    rotation in ReduceDiag (tile, tile, batch) of the reduction graph, a singular
+    pivot in SolveTile (tile, tile, batch) -- MergedSolveBacktransform (0, 0,
+    batch) for tile 0 -- of the substitution graph; ``seq`` by the graphs'
+    construction order (scheduler.py:120-179: batches outermost, tile columns
+    right to left, the diagonal node first, then one node per tile row)."""
+    N = n_tiles
+    seq = None
+    if N is not None:
+        before = sum(1 + t for t in range(tile + 1, N))  # nodes of the columns to the right
+        if phase_singular:
+            per_batch = sum(1 + t for t in range(1, N)) + 1
+            seq = batch * per_batch + (before if tile > 0 else per_batch - 1)
+        else:
+            per_batch = sum(1 + t for t in range(N))
+            seq = batch * per_batch + before
+    if not phase_singular:
+        return TaskNode("ReduceDiag", (tile, tile, batch), seq)
+    if tile == 0:
+        return TaskNode("MergedSolveBacktransform", (0, 0, batch), seq)
+    return TaskNode("SolveTile", (tile, tile, batch), seq)
+
+
 class HessenbergMatrix:
     """Read-only real upper Hessenberg matrix (core.py:60-98 semantics)."""
 

@@ -96,7 +96,7 @@ class ShardExchange:
     def any_remaining(self, count):
         return sum(self._collect(int(count))) > 0
 
-    def failures(self, attempt, fr, rr, fc, rc, b_c):
+    def failures(self, attempt, fr, rr, fc, rc, b_c, n_tiles=None):
         """All ranks' failure codes of this attempt, placed at their position
         in the reference's remaining-shift order; raises the first failure
         (solver.raise_first_failure) on every rank alike."""
@@ -111,7 +111,7 @@ class ShardExchange:
         R = sorted((g, c) for x in alls for g, c in zip(x[0], x[1]))
         C = sorted((g, c) for x in alls for g, c in zip(x[2], x[3]))
         codes = np.array([c for _, c in R] + [c for _, c in C], dtype=np.int64)
-        raise_first_failure(codes, b_c, [(0, len(R)), (len(R), len(R) + len(C))])
+        raise_first_failure(codes, b_c, [(0, len(R)), (len(R), len(R) + len(C))], n_tiles=n_tiles)
 
     def collect(self, payload):
         return self._collect(payload)

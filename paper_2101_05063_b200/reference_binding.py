@@ -74,13 +74,22 @@ def solve_group_b200(h, grid, eigs, b, config, workspace, cplx):
         out, _ = solve_group(dh, None, lam.astype(np.float64), B, grid.b_r, robust=True,
                              mode="eigvec", b_c=config.b_c)
     if out.nfail:
+        # the reference's executor re-raises the kernel's error as TaskError with
+        # the failing node (scheduler.py:182-187, 211-214): the same here, in the
+        # reference's own classes
         try:
-            raise_first_failure(out.fail.cpu().numpy(), config.b_c, [(0, m)])
-        except _core.SingularSystemError as e:
-            cls = _ref_module(h, "SingularSystemError")
-            raise cls(str(e), shift_index=e.shift_index, local_index=e.local_index) from None
-        except _core.StructuralViolationError as e:
-            raise _ref_module(h, "StructuralViolationError")(str(e)) from None
+            raise_first_failure(out.fail.cpu().numpy(), config.b_c, [(0, m)], n_tiles=grid.N)
+        except _core.TaskError as e:
+            if isinstance(e, _core.SingularSystemError):
+                cause = _ref_module(h, "SingularSystemError")(
+                    str(e.cause), shift_index=e.shift_index, local_index=e.local_index)
+            else:
+                cause = _ref_module(h, "StructuralViolationError")(str(e.cause))
+            sched = sys.modules.get(type(h).__module__.rsplit(".", 1)[0] + ".scheduler")
+            if sched is None or not hasattr(sched, "TaskError"):
+                raise cause from None
+            node = sched.TaskNode(e.node.kind, e.node.coords, seq=e.node.seq)
+            raise sched.TaskError(node, cause) from cause
     X = out.X.cpu().numpy()
     x = (X[0::2] + 1j * X[1::2]).T.copy() if cplx else X.T.copy()
     aexp = out.alpha_exp.cpu().numpy()

@@ -22,8 +22,11 @@ from .core import (
     HessenbergMatrix,
     ScalingMatrix,
     SingularSystemError,
+    SingularTaskError,
     SolutionBlock,
+    StructuralTaskError,
     StructuralViolationError,
+    task_node_of_failure,
 )
 
 MAX_TILE = 128  # b_r limit of the GPU path (one warp holds a tile column)
@@ -465,7 +468,7 @@ def _check_h(hm):
         raise ConfigError("matrix must be unreduced (nonzero subdiagonal)")
 
 
-def raise_first_failure(fail_codes, b_c, kinds):
+def raise_first_failure(fail_codes, b_c, kinds, n_tiles=None):
     """Raise the exception the reference would raise first.
 
     ``fail_codes`` per shift of one solve call (inviter/backsolve call order),
@@ -474,6 +477,13 @@ def raise_first_failure(fail_codes, b_c, kinds):
     (tiled_reduce runs before _substitute), batches in order, tile columns
     right to left, rows bottom-up within a kernel, then the batch-local shift
     (scheduler.py:189-219, numba_backend.py:79-106, 138-192).
+
+    What is raised is what the reference's caller sees: the executor's
+    ``TaskError`` (scheduler.py:182-187) naming the failing graph node, with
+    the kernel's ``SingularSystemError`` / ``StructuralViolationError`` as its
+    ``cause`` / ``__cause__`` -- as ``SingularTaskError`` /
+    ``StructuralTaskError`` (core.py here), which are instances of both.
+    ``n_tiles`` (the grid's N) gives the node its ``seq``.
     """
     codes = np.asarray(fail_codes, dtype=np.int64)
     best = None
@@ -498,14 +508,17 @@ def raise_first_failure(fail_codes, b_c, kinds):
             break
     if best is None:
         return
-    phase, _b, _t, _r, _l, q, tile, row = best
+    phase, batch, _t, _r, _l, q, tile, row = best
+    node = task_node_of_failure(phase == _KIND_SINGULAR, int(tile), int(batch), n_tiles)
     if phase == _KIND_DEGENERATE:
-        raise StructuralViolationError(
+        cause = StructuralViolationError(
             f"degenerate rotation in tile column {tile} at local row {row}, "
             f"shift {q} (both pivot entries are zero)")
-    raise SingularSystemError(
+        raise StructuralTaskError(node, cause) from cause
+    cause = SingularSystemError(
         f"singular triangular factor for shift {q} (local row {row})",
         shift_index=int(q), local_index=int(row))
+    raise SingularTaskError(node, cause) from cause
 
 
 def solve_group(h, eigs_cplx, eigs_real, b, b_r, *, robust=True, mode="eigvec", b_c=32,

@@ -49,9 +49,11 @@ def test_singular_shifts_raise_like_reference(dev):
     same error or return a finite result, and the inverse-iteration driver
     a converged eigenvector with residual <= 10 n eps.
     """
-    from paper_2101_05063_b200 import InviterConfig, SingularSystemError, chsrq3, dhsrq3, hsrq3in
+    from paper_2101_05063_b200 import (InviterConfig, SingularSystemError, TaskError, chsrq3,
+                                       dhsrq3, hsrq3in)
 
     g = golden("singular")
+    kinds = [str(k) for k in g["node_kinds"]]
     exact = 0
     for t in g["tags"]:
         h, lam = g[f"{t}_h"], g[f"{t}_lam"]
@@ -59,11 +61,19 @@ def test_singular_shifts_raise_like_reference(dev):
         n = h.shape[0]
         b = np.ones((n, lam.size)) + (0j if cplx else 0)
         f = chsrq3 if cplx else dhsrq3
-        for b_r, b_c, shift, row in g[f"{t}_hits"]:
+        for (b_r, b_c, shift, row), node, msg in zip(g[f"{t}_hits"], g[f"{t}_nodes"],
+                                                     g[f"{t}_messages"]):
             if b_r >= n:
                 with pytest.raises(SingularSystemError) as e:
                     f(h, lam, b, b_r=int(b_r), b_c=int(b_c))
                 assert (e.value.shift_index, e.value.local_index) == (shift, row)
+                # ... raised as the reference's caller sees it: the executor's
+                # TaskError naming the failing node (scheduler.py:182-187)
+                err = e.value
+                assert isinstance(err, TaskError) and err.__cause__ is err.cause
+                assert err.node.kind == kinds[node[0]]
+                assert tuple(err.node.coords) == tuple(int(v) for v in node[1:4])
+                assert err.node.seq == node[4] and str(err) == str(msg)
                 exact += 1
                 continue
             try:

@@ -9,8 +9,8 @@ Where it is absent the tests skip.  With ``hessrq.inviter._solve_group``
 routed to ``solve_group_b200``, the reference's ``hsrq3in`` / ``dhsrq3in`` /
 ``chsrq3in`` / ``_iterate`` (inviter.py:109-254: restarts, convergence,
 grouping, ordering -- all reference code) must reproduce the golden outputs
-of the reference's CPU run, and exactly singular shifts must raise the
-reference's own SingularSystemError with its indices.
+of the reference's CPU run, and exactly singular shifts must raise what the
+reference raises: its own TaskError around its SingularSystemError.
 """
 
 import os
@@ -101,20 +101,30 @@ def test_reference_config1_on_the_b200_seam(inviter):
 
 
 def test_reference_singular_shift_raises_reference_error(inviter):
-    """hsrq3in on an exactly singular shift: the reference's own exception
-    class with the reference's indices (or, across tiles, a converged vector:
-    test_gpu_configs.py documents why)."""
+    """hsrq3in on an exactly singular shift: what the reference's caller sees --
+    the reference's own TaskError (scheduler.py:182-187) with the node, message
+    and SingularSystemError cause of the reference's CPU run (or, across
+    tiles, a converged vector: test_gpu_configs.py documents why)."""
     import hessrq.core as rcore
+    import hessrq.scheduler as rsched
 
     g = golden("singular")
+    kinds = [str(k) for k in g["node_kinds"]]
     seen = 0
     for t in g["tags"]:
         h, lam = g[f"{t}_h"], g[f"{t}_lam"]
         want = tuple(g[f"{t}_inviter"])
+        node = g[f"{t}_inviter_node"]
         try:
             r = inviter.hsrq3in(h, np.array([lam[1]]), inviter.InviterConfig(b_r=3, b_c=2))
-        except rcore.SingularSystemError as e:
-            assert (e.shift_index, e.local_index) == want
+        except rsched.TaskError as e:
+            assert type(e) is rsched.TaskError and isinstance(e.cause, rcore.SingularSystemError)
+            assert e.__cause__ is e.cause
+            assert (e.cause.shift_index, e.cause.local_index) == want
+            assert isinstance(e.node, rsched.TaskNode) and e.node.kind == kinds[node[0]]
+            assert tuple(e.node.coords) == tuple(int(v) for v in node[1:4])
+            assert e.node.seq == node[4]
+            assert str(e) == str(g[f"{t}_inviter_message"])
             seen += 1
         else:
             assert r.converged[0]

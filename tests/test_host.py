@@ -69,6 +69,54 @@ def test_first_failure_follows_reference_order():
     raise_first_failure(np.zeros(4, dtype=np.int64), 4, [(0, 4)])  # no failure: no raise
 
 
+def test_failure_is_the_references_task_error():
+    """A caller of the reference catches the executor's TaskError naming the
+    failing graph node, with the kernel's error as cause (scheduler.py:182-187,
+    211-214).  Same here -- node kind, coords, seq and message pinned to what
+    the live reference raised (golden singular.npz: its dhsrq3 / chsrq3 calls
+    and its graph builders) -- and the error is also a SingularSystemError /
+    StructuralViolationError instance."""
+    from conftest import golden
+    from paper_2101_05063_b200 import TaskError
+    from paper_2101_05063_b200.core import task_node_of_failure
+
+    g = golden("singular")
+    kinds = [str(k) for k in g["node_kinds"]]
+    n = 8
+    for t in g["tags"]:
+        for (b_r, b_c, q, row), node, msg in zip(g[f"{t}_hits"], g[f"{t}_nodes"],
+                                                 g[f"{t}_messages"]):
+            codes = np.zeros(4, dtype=np.int64)
+            codes[q] = _code(2, int(node[1]), int(row))
+            with pytest.raises(TaskError) as e:
+                raise_first_failure(codes, int(b_c), [(0, 4)], n_tiles=-(-n // int(b_r)))
+            err = e.value
+            assert isinstance(err, SingularSystemError) and isinstance(err.cause, SingularSystemError)
+            assert err.__cause__ is err.cause
+            assert (err.shift_index, err.local_index) == (q, row)
+            assert (err.cause.shift_index, err.cause.local_index) == (q, row)
+            assert err.node.kind == kinds[node[0]]
+            assert tuple(err.node.coords) == tuple(int(v) for v in node[1:4])
+            assert err.node.seq == node[4]
+            assert str(err) == str(msg)
+    # node positions in the reference's reduction / substitution graphs
+    for N in range(1, 6):
+        for b in range(3):
+            for tile in range(N):
+                assert task_node_of_failure(False, tile, b, N).seq == g["dag_reduce_seq"][N - 1, b, tile]
+                nd = task_node_of_failure(True, tile, b, N)
+                assert nd.seq == g["dag_solve_seq"][N - 1, b, tile]
+                assert nd.kind == ("MergedSolveBacktransform" if tile == 0 else "SolveTile")
+    codes = np.zeros(6, dtype=np.int64)
+    codes[5] = _code(1, 2, 7)  # degenerate rotation in tile column 2, batch 1 (b_c = 4)
+    with pytest.raises(TaskError) as e:
+        raise_first_failure(codes, 4, [(0, 6)], n_tiles=3)
+    assert isinstance(e.value, StructuralViolationError)
+    assert e.value.node.kind == "ReduceDiag" and e.value.node.coords == (2, 2, 1)
+    assert str(e.value) == ("task ReduceDiag at (2, 2, 1) failed: degenerate rotation in tile "
+                            "column 2 at local row 7, shift 5 (both pivot entries are zero)")
+
+
 def test_shards_balance_flop_cost():
     rc, cc = shard_bounds(3790, 6105, 8)
     assert rc[0] == cc[0] == 0 and rc[-1] == 3790 and cc[-1] == 6105

@@ -308,9 +308,15 @@ def gen_inviter():
     save("inviter", **store)
 
 
+_NODE_KINDS = ["ReduceDiag", "SolveTile", "MergedSolveBacktransform"]
+
+
 def _reference_error(f):
-    """The SingularSystemError a reference call raises (unwrapping TaskError), or None."""
+    """The SingularSystemError a reference call raises (unwrapping TaskError), or None.
+    The error carries ``task`` = (kind index in _NODE_KINDS, tile_i, tile_j, batch,
+    seq) of the TaskError's node (scheduler.py:182-187) and ``task_message``."""
     from hessrq.core import SingularSystemError
+    from hessrq.scheduler import TaskError
 
     try:
         f()
@@ -320,6 +326,9 @@ def _reference_error(f):
             c = c.__cause__
         if c is None:
             raise
+        assert isinstance(e, TaskError) and e.cause is c and e.__cause__ is c
+        c.task = (_NODE_KINDS.index(e.node.kind),) + tuple(e.node.coords) + (e.node.seq,)
+        c.task_message = str(e)
         return c
     return None
 
@@ -356,11 +365,13 @@ def gen_singular():
                      else np.array([lr + 0.25, lr, lr + 0.5, lr], dtype=float))
             b = np.ones((n, 4)) + (0j if cplx else 0)
             f = chsrq3 if cplx else dhsrq3
-            hit = []
+            hit, nodes, msgs = [], [], []
             for b_r, b_c in ((8, 4), (3, 2), (2, 1)):
                 e = _reference_error(lambda: f(h, lam_v, b, b_r=b_r, b_c=b_c))
                 if e is not None:
                     hit.append((b_r, b_c, e.shift_index, e.local_index))
+                    nodes.append(e.task)
+                    msgs.append(e.task_message)
             if not hit:
                 continue
             ei = _reference_error(lambda: hsrq3in(h, np.array([z]), InviterConfig(b_r=3, b_c=2)))
@@ -371,13 +382,92 @@ def gen_singular():
             store[f"{t}_hits"] = np.array(hit, dtype=np.int64)
             store[f"{t}_inviter"] = np.array(
                 [-1, -1] if ei is None else [ei.shift_index, ei.local_index], dtype=np.int64)
+            # the TaskError the caller actually sees (scheduler.py:182-187, 211-214):
+            # node (kind index, tile_i, tile_j, batch, seq) and its message, per hit
+            store[f"{t}_nodes"] = np.array(nodes, dtype=np.int64)
+            store[f"{t}_messages"] = np.array(msgs)
+            store[f"{t}_inviter_node"] = np.array(
+                [-1] * 5 if ei is None else list(ei.task), dtype=np.int64)
+            store[f"{t}_inviter_message"] = np.array("" if ei is None else ei.task_message)
             tags.append(t)
             if cplx:
                 want_cplx -= 1
             else:
                 want_real -= 1
             break
-    save("singular", tags=np.array(tags), **store)
+    # seq of the nodes a failure can surface in, from the reference's own graph
+    # builders (scheduler.py:120-179): [N - 1, batch, tile] for N = 1..5, 3 batches
+    from types import SimpleNamespace
+
+    from hessrq.scheduler import build_reduce_dag, build_solve_dag
+
+    rseq = -np.ones((5, 3, 5), dtype=np.int64)
+    sseq = -np.ones((5, 3, 5), dtype=np.int64)
+    for N in range(1, 6):
+        gr = build_reduce_dag(SimpleNamespace(N=N), 3)
+        gs = build_solve_dag(SimpleNamespace(N=N), 3)
+        for node in gr.nodes:
+            if node.kind == "ReduceDiag":
+                rseq[N - 1, node.coords[2], node.coords[0]] = node.seq
+        for node in gs.nodes:
+            if node.kind in ("SolveTile", "MergedSolveBacktransform"):
+                sseq[N - 1, node.coords[2], node.coords[0]] = node.seq
+    save("singular", tags=np.array(tags), node_kinds=np.array(_NODE_KINDS), dag_reduce_seq=rseq,
+         dag_solve_seq=sseq, **store)
+
+
+def gen_edge():
+    """Edge inputs of the inverse-iteration drivers (inviter.py:109-254): n = 1,
+    2, 3, a one-row ragged last tile (n = 33, b_r = 32), one shift of either
+    kind, only Im < 0 shifts, a repeated shift, the caller's mixed order, an
+    empty selection -- what the reference returns or raises for each."""
+    rng = np.random.default_rng(11)
+    store, tags = {}, []
+
+    def case(tag, h, eigs, b_r, fn=hsrq3in):
+        store[f"{tag}_h"] = np.asfortranarray(h)
+        store[f"{tag}_eigs"] = np.asarray(eigs)
+        store[f"{tag}_br"] = np.array(b_r)
+        store[f"{tag}_fn"] = np.array(fn.__name__)
+        try:
+            r = fn(h, eigs, InviterConfig(b_r=b_r))
+        except Exception as e:  # noqa: BLE001 - the reference's error is the fixture
+            store[f"{tag}_error"] = np.array(type(e).__name__)
+            store[f"{tag}_message"] = np.array(str(e))
+        else:
+            store[f"{tag}_error"] = np.array("")
+            v = np.asarray(r.vectors)
+            store[f"{tag}_vectors"] = v.astype(np.complex128)
+            store[f"{tag}_conv"] = np.asarray(r.converged)
+            store[f"{tag}_restarts"] = np.asarray(r.restarts)
+        tags.append(tag)
+
+    def hess(n):
+        h = np.triu(rng.standard_normal((n, n)), -1)
+        for i in range(1, n):
+            h[i, i - 1] = abs(h[i, i - 1]) + 0.1
+        return h
+
+    case("n1_exact", np.array([[2.0]]), np.array([2.0]), 1)
+    case("n1_near", np.array([[2.0]]), np.array([2.0 + 1e-9]), 1)
+    h2 = hess(2)
+    case("n2_all", h2, np.linalg.eigvals(h2), 2)
+    h3 = hess(3)
+    case("n3_all", h3, np.linalg.eigvals(h3), 2)  # ragged: tiles of 2 + 1
+    h33 = hess(33)
+    ev = np.linalg.eigvals(h33)
+    er, ec = ev[ev.imag == 0], ev[ev.imag > 0]
+    case("n33_ragged", h33, ev, 32)
+    case("n33_one_real", h33, er[:1].real, 32, dhsrq3in)
+    case("n33_one_cplx", h33, ec[:1], 32, chsrq3in)
+    case("n33_conj_only", h33, np.conj(ec[:3]), 32)
+    case("n33_repeated", h33, np.array([ec[0], er[0], ec[0], er[0]]), 32)
+    case("n33_mixed_order", h33, np.concatenate([np.conj(ec[:2]), er[:2], ec[:2]])[::-1], 32)
+    case("n33_empty", h33, ev[:0], 32)
+    case("n33_empty_real", h33, er[:0].real, 32, dhsrq3in)
+    case("n33_real_as_complex_api", h33, er[:2].astype(complex), 32, chsrq3in)
+    case("n33_complex_to_real_api", h33, ec[:1], 32, dhsrq3in)
+    save("edge", tags=np.array(tags), **store)
 
 
 def gen_backtransform():
