@@ -11,6 +11,7 @@ from .core import (
     ConfigError,
     HessenbergMatrix,
     HessrqError,
+    OverflowBudget,
     RunStats,
     ScalingMatrix,
     SingularSystemError,
@@ -19,6 +20,9 @@ from .core import (
     TaskError,
     TaskNode,
     TileGrid,
+    Workspace,
+    deinterleave_complex,
+    interleave_complex,
 )
 from .inviter import (
     EigvecResult,
@@ -31,6 +35,7 @@ from .inviter import (
 )
 from .backsolve import chsrq3, dhsrq3
 from .henry import henry_rq_solve
+from .hessenberg import backmultiply, householder_hessenberg, hsrq3in_dense
 from . import flops
 
 __version__ = "0.1.0"

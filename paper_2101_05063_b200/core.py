@@ -129,6 +129,9 @@ class HessenbergMatrix:
             return True
         return bool(np.all(np.diagonal(self.data, -1) != 0.0))
 
+    def subdiagonal(self):
+        return np.diagonal(self.data, -1).copy()
+
     def __repr__(self):
         return f"HessenbergMatrix(n={self.n})"
 
@@ -148,9 +151,68 @@ class TileGrid:
         self.ranges = [(s, min(s + b_r, n)) for s in range(0, n, b_r)]
         self.N = len(self.ranges)
 
+    def tile_of(self, i):
+        return i // self.b_r
+
+    def tile_slice(self, t):
+        s, e = self.ranges[t]
+        return slice(s, e)
+
+    def __repr__(self):
+        return f"TileGrid(n={self.n}, b_r={self.b_r}, N={self.N})"
+
     @property
     def tile_ends(self):
         return np.array([e for _s, e in self.ranges], dtype=np.int64)
+
+
+_DBL_MAX = float(np.finfo(np.float64).max)
+
+
+@dataclass(frozen=True)
+class OverflowBudget:
+    """The working overflow threshold omega (overflow.py:30-47): the ``budget=``
+    argument of dhsrq3 / chsrq3.  Default: the true overflow limit over two and
+    over the tile height."""
+
+    omega: float
+    safety_divisor: int = 1
+
+    def __post_init__(self):
+        if not (0.0 < self.omega <= _DBL_MAX / 2.0):
+            raise ValueError(f"omega={self.omega} outside (0, maxfloat/2]")
+        if self.omega * self.safety_divisor > _DBL_MAX:
+            raise ValueError("omega * safety_divisor exceeds the representable range")
+
+    @classmethod
+    def for_tile_rows(cls, b_r):
+        return cls(omega=_DBL_MAX / 2.0 / b_r, safety_divisor=int(b_r))
+
+    @classmethod
+    def for_grid(cls, grid):
+        return cls.for_tile_rows(grid.b_r)
+
+
+class Workspace:
+    """The ``workspace=`` argument of the drivers (core.py:263-283): host scratch
+    keyed by role, and the high-water mark of cross-over storage in reals.  The
+    GPU path keeps its cross-over block on the device (O(n cols), DESIGN.md);
+    ``peak_crossover_reals`` reports the reference's figure, n N cols, so caps
+    written against the reference keep their meaning."""
+
+    def __init__(self):
+        self._bufs = {}
+        self.peak_crossover_reals = 0
+
+    def take(self, key, shape, dtype=np.float64, crossover=False):
+        size = int(np.prod(shape))
+        buf = self._bufs.get(key)
+        if buf is None or buf.size < size or buf.dtype != np.dtype(dtype):
+            buf = np.empty(size, dtype=dtype)
+            self._bufs[key] = buf
+        if crossover:
+            self.peak_crossover_reals = max(self.peak_crossover_reals, size)
+        return buf[:size].reshape(shape)
 
 
 @dataclass
@@ -184,6 +246,23 @@ class SolutionBlock:
     flops: dict = field(default_factory=dict)
     alpha_exp: np.ndarray | None = None
     log2_norms: np.ndarray | None = None
+
+
+def interleave_complex(z):
+    """(n, m) complex -> (n, 2m) float with re/im in adjacent columns (core.py:286-292)."""
+    z = np.asarray(z, dtype=np.complex128)
+    out = np.empty((z.shape[0], 2 * z.shape[1]), dtype=np.float64)
+    out[:, 0::2] = z.real
+    out[:, 1::2] = z.imag
+    return out
+
+
+def deinterleave_complex(x):
+    """(n, 2m) float interleaved -> (n, m) complex (core.py:295-300)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape[1] % 2:
+        raise ConfigError("interleaved array must have an even column count")
+    return x[:, 0::2] + 1j * x[:, 1::2]
 
 
 class RunStats:

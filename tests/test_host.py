@@ -166,3 +166,88 @@ def test_verify_suite_matrices_match_reference_fixtures():
     h2, h3 = paper_h(60, -60).data, paper_h(60, 0.5).data
     assert any(np.array_equal(h, h2) for h in hs.values())
     assert any(np.array_equal(h, h3) for h in hs.values())
+
+
+def test_api_types_of_the_reference_surface():
+    """The types a caller of the reference's path constructs or receives
+    (core.py:105-129, 263-300; overflow.py:30-47) exist here with the same
+    constructor checks, methods and values."""
+    import paper_2101_05063_b200 as P
+
+    g = P.TileGrid(300, 128)
+    assert (g.n, g.b_r, g.N, g.ranges) == (300, 128, 3, [(0, 128), (128, 256), (256, 300)])
+    assert g.tile_of(255) == 1 and g.tile_slice(2) == slice(256, 300)
+    assert repr(g) == "TileGrid(n=300, b_r=128, N=3)"
+    with pytest.raises(ConfigError):
+        P.TileGrid(10, 11)
+    b = P.OverflowBudget.for_grid(g)
+    dmax = float(np.finfo(np.float64).max)
+    assert b.omega == dmax / 2.0 / 128 and b.safety_divisor == 128
+    assert P.OverflowBudget.for_tile_rows(64) == P.OverflowBudget(dmax / 2.0 / 64, 64)
+    for bad in (0.0, dmax):
+        with pytest.raises(ValueError):
+            P.OverflowBudget(bad)
+    with pytest.raises(ValueError):
+        P.OverflowBudget(dmax / 2.0, 4)
+    w = P.Workspace()
+    a = w.take("x", (3, 4), crossover=True)
+    assert a.shape == (3, 4) and w.peak_crossover_reals == 12
+    assert w.take("x", (2, 2)).base is a.base  # reused allocation
+    z = np.array([[1 + 2j, 3 - 4j]])
+    assert np.array_equal(P.interleave_complex(z), [[1.0, 2.0, 3.0, -4.0]])
+    assert np.array_equal(P.deinterleave_complex(P.interleave_complex(z)), z)
+    with pytest.raises(ConfigError):
+        P.deinterleave_complex(np.zeros((2, 3)))
+    h = P.HessenbergMatrix(np.triu(np.arange(16.0).reshape(4, 4), -1))
+    assert np.array_equal(h.subdiagonal(), [4.0, 9.0, 14.0]) and h.is_unreduced()
+
+
+def test_api_surface_matches_installed_reference():
+    """With the reference importable (baseline/_ref in the build container):
+    every driver accepts the reference's positional / keyword arguments, and the
+    config / result types carry at least the reference's fields with the same
+    defaults, in the same order."""
+    import dataclasses
+    import inspect
+    import os
+    import sys
+
+    from conftest import ROOT
+
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "hessrq")):
+        pytest.skip("reference not installed under baseline/_ref")
+    sys.path.insert(0, ref)
+    try:
+        import hessrq.backsolve as rb
+        import hessrq.core as rc
+        import hessrq.inviter as ri
+        import hessrq.scheduler as rs
+    finally:
+        sys.path.remove(ref)
+    import paper_2101_05063_b200 as P
+
+    for name, rf in (("hsrq3in", ri.hsrq3in), ("dhsrq3in", ri.dhsrq3in), ("chsrq3in", ri.chsrq3in),
+                     ("dhsrq3", rb.dhsrq3), ("chsrq3", rb.chsrq3), ("converged", ri.converged),
+                     ("starting_vector", ri.starting_vector)):
+        want = list(inspect.signature(rf).parameters.values())
+        got = list(inspect.signature(getattr(P, name)).parameters.values())
+        assert [(p.name, p.kind, p.default) for p in got[:len(want)]] == \
+               [(p.name, p.kind, p.default) for p in want], name
+        assert all(p.default is not inspect.Parameter.empty for p in got[len(want):]), name
+    for name, mod in (("InviterConfig", ri), ("EigvecResult", ri), ("SolutionBlock", rc)):
+        want = dataclasses.fields(getattr(mod, name))
+        got = dataclasses.fields(getattr(P, name))
+        for fw, fg in zip(want, got):
+            assert fw.name == fg.name, (name, fw.name, fg.name)
+            if fw.default is not dataclasses.MISSING:
+                assert fw.default == fg.default, (name, fw.name)
+    for cls in ("HessrqError", "ConfigError", "SingularSystemError", "StructuralViolationError"):
+        assert [b.__name__ for b in getattr(P, cls).__mro__] == \
+               [b.__name__ for b in getattr(rc, cls).__mro__], cls
+    assert [b.__name__ for b in P.TaskError.__mro__] == [b.__name__ for b in rs.TaskError.__mro__]
+    for cls, mod in (("TileGrid", rc), ("HessenbergMatrix", rc), ("ScalingMatrix", rc),
+                     ("Workspace", rc), ("TaskNode", rs)):
+        want = {m for m in dir(getattr(mod, cls)) if not m.startswith("_")}
+        got = {m for m in dir(getattr(P, cls)) if not m.startswith("_")}
+        assert want <= got, (cls, want - got)
