@@ -83,6 +83,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CL_THREADS, CL_MINB)
     for (int i = 0; i < 4; i++)
       cp_async16(&sm.u.pipe.B[stage][nn + 16 * i][k2], b + 16 * i * KP, true);
   };
+  // Remote shared memory may only be touched once the peer CTA is known to
+  // run: arrive at the cluster barrier now, wait for it right before the
+  // push of the maxima (long satisfied by then, so the wait costs nothing).
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   load(0, 0);
   cp_commit();
   if (g_panel_prefetch) {  // this CTA's epilogue tiles (X, Cr: 32 columns x 64 rows) towards L2
@@ -246,6 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CL_THREADS, CL_MINB)
     mr0 = fmax(mr0, __shfl_xor_sync(0xffffffffu, mr0, o));
     mr1 = fmax(mr1, __shfl_xor_sync(0xffffffffu, mr1, o));
   }
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // the peer CTA has started
   if (rp == 0) {
     sm.red[0][cl0] = peer.redp[0][cl0] = dkey(mb0);
     sm.red[0][cl0 + 1] = peer.redp[0][cl0 + 1] = dkey(mb1);
