@@ -566,28 +566,49 @@ inline dim3 gemv_t_grid(int m, int n, int* rs_rows) {
 // with the panel correction and the reflector's scale (DLAHR2's Y column).
 // Four lanes per row: lane q adds chunks / columns q, q + 4, ... in order, the
 // four sums are combined as (0 + 1) + (2 + 3).  blockDim = 128 (32 rows).
+// With anext != NULL the same pass over the row of Y also applies the right
+// update of the panel's NEXT column, anext -= Y[:, :p + 1] vnext[:p + 1]^T
+// (vnext[k] = V[j + 1, k] at stride ldvn; Y[:, p] is the column just formed),
+// which would otherwise be a launch of its own per column.
 __global__ void __launch_bounds__(128) k_gemv_n_reduce_y(int m, int nchunk, const double* part,
                                                          const double* Y, int64_t ldy, int p,
                                                          const double* w, const double* tau,
-                                                         double* y) {
-  __shared__ double ws[64];
+                                                         double* y, double* anext,
+                                                         const double* vnext, int64_t ldvn) {
+  __shared__ double ws[64], vs[65];
   if (threadIdx.x < p) ws[threadIdx.x] = w[threadIdx.x];
+  if (anext && threadIdx.x <= p) vs[threadIdx.x] = vnext[(int64_t)threadIdx.x * ldvn];
   __syncthreads();
   // lanes of a quad differ in lane bits 3..4, so a warp's loads cover 8 consecutive rows
   const int lane = threadIdx.x & 31, q = lane >> 3;
   const int r = blockIdx.x * 32 + (threadIdx.x >> 5) * 8 + (lane & 7);
-  double s = 0.0, cor = 0.0;
+  double s = 0.0, cor = 0.0, upd = 0.0;
   if (r < m) {
 #pragma unroll 4
     for (int c = q; c < nchunk; c += 4) s += part[(int64_t)c * m + r];
+    if (anext) {
 #pragma unroll 4
-    for (int k = q; k < p; k += 4) cor += Y[r + (int64_t)k * ldy] * ws[k];
+      for (int k = q; k < p; k += 4) {
+        const double yk = Y[r + (int64_t)k * ldy];
+        cor += yk * ws[k];
+        upd += yk * vs[k];
+      }
+    } else {
+#pragma unroll 4
+      for (int k = q; k < p; k += 4) cor += Y[r + (int64_t)k * ldy] * ws[k];
+    }
   }
   s += __shfl_xor_sync(0xffffffffu, s, 8);
   cor += __shfl_xor_sync(0xffffffffu, cor, 8);
+  upd += __shfl_xor_sync(0xffffffffu, upd, 8);
   s += __shfl_xor_sync(0xffffffffu, s, 16);
   cor += __shfl_xor_sync(0xffffffffu, cor, 16);
-  if (r < m && q == 0) y[r] = *tau * (s - cor);
+  upd += __shfl_xor_sync(0xffffffffu, upd, 16);
+  if (r < m && q == 0) {
+    const double yr = *tau * (s - cor);
+    y[r] = yr;
+    if (anext) anext[r] -= upd + yr * vs[p];
+  }
 }
 
 // x = T x (trans = 0) or T^T x (trans = 1), T p x p upper (ldt), one block.

@@ -166,8 +166,8 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
       const int64_t j = j0 + i;
       double* aj = A + j * lda;
       if (i > 0) {
-        // right update of column j, rows s..: a_j -= Y[s:, :i] V[j, :i]^T
-        dgemv(false, (int)Ls, i, -1.0, Y + s, ldv, V + j, ldv, 1.0, aj + s, part, stream);
+        // (the right update of column j, rows s..: a_j -= Y[s:, :i] V[j, :i]^T, was
+        // applied by the previous column's k_gemv_n_reduce_y, in its pass over Y)
         // left update of rows j0+1.. : a -= V T^T V^T a  (u = T^T V^T a in one launch)
         k_gemv_t_trmv<<<gemv_t_grid((int)L, i, &rs_rows), 256, 0, stream>>>(
             (int)L, i, V + j0 + 1, ldv, aj + j0 + 1, u, T, nb, 1, nullptr, u, counter, ypart, rs_rows);
@@ -190,8 +190,10 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
           k_gemv_n_part<<<dim3((unsigned)((Ls + GV_ROWS - 1) / GV_ROWS), (unsigned)nchunk),
                           GV_THREADS, 0, stream>>>((int)Ls, nv, A + (j + 1) * lda + s, lda,
                                                    vi + j + 1, 1, part);
+        const bool nxt = i + 1 < pb;  // the panel's next column takes its right update here
         k_gemv_n_reduce_y<<<(unsigned)((Ls + 31) / 32), 128, 0, stream>>>(
-            (int)Ls, nchunk, part, Y + s, ldv, i, wv, tau + i, yi + s);
+            (int)Ls, nchunk, part, Y + s, ldv, i, wv, tau + i, yi + s,
+            nxt ? aj + lda + s : nullptr, V + j + 1, ldv);
       }
     }
     const int64_t c0 = j0 + pb, nc = n - c0;  // trailing columns
