@@ -30,7 +30,11 @@
 
 namespace {
 
-constexpr int HB_THREADS = 1024;
+// k_update_reflect: rows per CTA.  The last CTA's vector phase (n rows) sets
+// the time: n = 16000 reduce + Q 3.40 / 3.32 / 3.28 s at 256 / 512 / 1024.
+#ifndef UR_THREADS
+#define UR_THREADS 1024
+#endif
 constexpr int HB_NB = 64;  // panel width
 
 thread_local char g_herr[256] = "";
@@ -50,22 +54,58 @@ __device__ double block_sum(double v, double* red) {
   return red[32];
 }
 
-// Reflector of column j (testprob.py:160-172), one CTA.  a = column j of A
-// (length n, updated in place: a[j+1] = alpha, a[j+2:] = 0 unless skipped);
-// vcol = column i of V (length n: zero above row j+1); tau[i] / ntau[i] =
-// 2 / -2 (0 when skipped); T[i, i] = tau.
-__global__ void __launch_bounds__(HB_THREADS) k_reflector(double* a, int64_t n, int64_t j,
-                                                          double* vcol, double* tau, double* ntau,
-                                                          double* Tii) {
+// Left update of column j by the panel's earlier reflectors, a[j0+1:] -=
+// V[:, :i] u, fused with the reflector of the column (testprob.py:160-172).
+// One thread per row of a[j0+1:] (UR_THREADS-thread CTAs); each CTA adds its rows'
+// share of tail = x[1:].x[1:] (x = a[j+1:]) to `rpart`; the CTA that finishes
+// last (device counter) adds the shares in CTA order and forms the reflector:
+// skipped when tail == 0 (a Hessenberg column stays untouched, bit for bit),
+// alpha = -sign(x0) hypot(x0, sqrt(tail)), v = (x - alpha e1) / ||.|| with
+// ||.||^2 = v0^2 + tail (numpy's unscaled norm, as the reference).  Writes
+// vcol = column i of V (length n: zero above row j+1), a[j+1] = alpha,
+// a[j+2:] = 0, tau[i] / ntau[i] = 2 / -2 (0 when skipped), T[i, i] = tau.
+__global__ void __launch_bounds__(UR_THREADS) k_update_reflect(
+    double* a, int64_t n, int64_t j, int64_t j0, int i, const double* V, int64_t ldv,
+    const double* u, double* vcol, double* tau, double* ntau, double* Tii, double* rpart,
+    unsigned* counter) {
   __shared__ double red[33];
-  const int64_t m = n - j - 1;  // x = a[j+1 : n]
-  const double* x = a + j + 1;
+  __shared__ double us[64];
+  __shared__ bool last;
+  if (threadIdx.x < i) us[threadIdx.x] = u[threadIdx.x];
+  __syncthreads();
+  const int64_t r = j0 + 1 + (int64_t)blockIdx.x * UR_THREADS + threadIdx.x;
   double t = 0.0;
-  for (int64_t r = 1 + threadIdx.x; r < m; r += blockDim.x) t += x[r] * x[r];
-  const double tail = block_sum(t, red);
-  const double x0 = x[0];
-  if (tail == 0.0) {  // column already reduced: identity reflector, nothing written
-    for (int64_t r = threadIdx.x; r < n; r += blockDim.x) vcol[r] = 0.0;
+  if (r < n) {
+    double ar = a[r];
+    if (i > 0) {
+      const double* vr = V + r;
+      double s0 = 0.0, s1 = 0.0;
+      int k = 0;
+      for (; k + 2 <= i; k += 2) {
+        s0 += vr[(int64_t)k * ldv] * us[k];
+        s1 += vr[(int64_t)(k + 1) * ldv] * us[k + 1];
+      }
+      if (k < i) s0 += vr[(int64_t)k * ldv] * us[k];
+      ar -= s0 + s1;
+      a[r] = ar;
+    }
+    if (r >= j + 2) t = ar * ar;
+  }
+  t = block_sum(t, red);
+  if (threadIdx.x == 0) {
+    rpart[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *counter = 0u;  // ready for the next launch
+  double tail = 0.0;
+  for (unsigned c = 0; c < gridDim.x; c++) tail += __ldcg(rpart + c);  // CTA order: deterministic
+  const double x0 = __ldcg(a + j + 1);
+  if (tail == 0.0) {  // column already reduced: identity reflector, a stays as it is
+    for (int64_t q = threadIdx.x; q < n; q += blockDim.x) vcol[q] = 0.0;
     if (threadIdx.x == 0) {
       *tau = 0.0;
       *ntau = -0.0;
@@ -76,16 +116,16 @@ __global__ void __launch_bounds__(HB_THREADS) k_reflector(double* a, int64_t n, 
   const double nrm = hsrq::ghypot(x0, sqrt(tail));
   const double alpha = x0 >= 0.0 ? -nrm : nrm;
   const double v0 = x0 - alpha;
-  // v /= np.linalg.norm(v): numpy's unscaled sqrt(v.v), and v.v = v0^2 + tail
-  // (the reference forms tail the same unscaled way, testprob.py:163)
   const double vn = sqrt(v0 * v0 + tail);
-  for (int64_t r = threadIdx.x; r < n; r += blockDim.x) {
+  // (rows written by other CTAs are read past L1; each row is read and rewritten by one thread)
+  for (int64_t q = threadIdx.x; q < n; q += blockDim.x) {
     double v = 0.0;
-    if (r > j) v = (r == j + 1 ? v0 : a[r]) / vn;
-    vcol[r] = v;
+    if (q > j) {
+      v = (q == j + 1 ? v0 : __ldcg(a + q)) / vn;
+      a[q] = q == j + 1 ? alpha : 0.0;
+    }
+    vcol[q] = v;
   }
-  __syncthreads();  // every read of a[j+1:] precedes the writes below
-  for (int64_t r = j + 1 + threadIdx.x; r < n; r += blockDim.x) a[r] = r == j + 1 ? alpha : 0.0;
   if (threadIdx.x == 0) {
     *tau = 2.0;
     *ntau = -2.0;
@@ -171,11 +211,11 @@ int64_t hsrq_hessenberg_reduce(double* A, int64_t lda, double* Q, int64_t ldq, i
         // left update of rows j0+1.. : a -= V T^T V^T a  (u = T^T V^T a in one launch)
         k_gemv_t_trmv<<<gemv_t_grid((int)L, i, &rs_rows), 256, 0, stream>>>(
             (int)L, i, V + j0 + 1, ldv, aj + j0 + 1, u, T, nb, 1, nullptr, u, counter, ypart, rs_rows);
-        dgemv(false, (int)L, i, -1.0, V + j0 + 1, ldv, u, 1, 1.0, aj + j0 + 1, part, stream);
       }
+      // ... a -= V u for rows j0+1.., and the column's reflector, one launch
       double* vi = V + (size_t)i * ldv;
-      k_reflector<<<1, HB_THREADS, 0, stream>>>(aj, n, j, vi, tau + i, ntau + i,
-                                                 T + (size_t)i * nb + i);
+      k_update_reflect<<<(unsigned)((L + UR_THREADS - 1) / UR_THREADS), UR_THREADS, 0, stream>>>(
+          aj, n, j, j0, i, V, ldv, u, vi, tau + i, ntau + i, T + (size_t)i * nb + i, part, counter);
       if (!cu_ok(cudaGetLastError(), "reflector")) return HSRQ_ERR_CUDA;
       // Y[s:, i] = tau (A[s:, j+1:] v - Y[s:, :i] (V^T v)); T[:i, i] = -tau T[:i, :i] (V^T v)
       double* yi = Y + (size_t)i * ldv;
