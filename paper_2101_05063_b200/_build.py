@@ -73,7 +73,14 @@ def build(force=False, verbose=False, variant=None, defines=()):
     if not force and not variant and not stale():
         return LIB
     extra = [f"-D{d}" for d in defines]
-    objdir = os.path.join(HERE, "build", variant or "main")
+    # objects are cached per variant AND per define set (a build with extra
+    # -D flags must never be linked into the plain library later)
+    tag = variant or "main"
+    if extra:
+        import hashlib
+
+        tag += "-" + hashlib.sha1(" ".join(sorted(extra)).encode()).hexdigest()[:8]
+    objdir = os.path.join(HERE, "build", tag)
     os.makedirs(objdir, exist_ok=True)
     flags = [f for f in NVCC_FLAGS if f != "-shared"]
     jobs, objs = [], []
