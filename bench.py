@@ -228,6 +228,18 @@ class ReferenceCPU:
         return self.sr.size + self.sc.size, conv, time.perf_counter() - t0
 
 
+def ref_sample(args, nsteps):
+    """Shifts of each kind per step of the reference's CPU path: 128 + 128 = 256
+    (four full b_c = 32 batches per kind, so the reference's executor and its
+    BLAS work at their efficient sizes -- BASELINE.md §5 asks for >= 256; an 8 +
+    8 sample runs the same code at half the per-shift rate), reduced in steps
+    of 32 when many steps are asked for, so that the whole run stays within a
+    few minutes (about 13 s per 256-shift step on 16 host threads)."""
+    per = 128 if nsteps <= 10 else min(128, max(32, int(round(1280.0 / nsteps / 32.0)) * 32))
+    return (args.ref_real if args.ref_real is not None else per,
+            args.ref_cplx if args.ref_cplx is not None else per)
+
+
 def arm_config(cfg, n, m_r, m_c, b_r, world):
     """The workload description both arms print (bench contract `config`)."""
     return {
@@ -251,7 +263,7 @@ def run_reference(args):
 
     n = h.shape[0]
     if reference_available() and not args.port:
-        ref = ReferenceCPU(h, er, ec, b_r, args.ref_real, args.ref_cplx)
+        ref = ReferenceCPU(h, er, ec, b_r, *ref_sample(args, args.warmup + args.steps))
         kind, threads, sample = "reference", ref.workers, ref.sample
         dts, att, conv = [], 0, 0
         for i in range(args.warmup + args.steps):
@@ -610,7 +622,7 @@ def run_gpu(args):
         port = {"value": cnt / dt, "unit": "eigenvectors/s", "cores": threads, "kind": "port",
                 "sample": sample}
         if reference_available() and not args.port:
-            ref = ReferenceCPU(h, er, ec, b_r, args.ref_real, args.ref_cplx)
+            ref = ReferenceCPU(h, er, ec, b_r, *ref_sample(args, 1))
             a, c, dt = ref.step()
             line["cpu_baseline"] = {"value": a / dt, "unit": "eigenvectors/s", "cores": ref.workers,
                                     "kind": "reference", "sample": ref.sample,
@@ -695,10 +707,12 @@ def main():
     ap.add_argument("--no-shards", action="store_true", help="skip the 2/4/8-way shard projection")
     ap.add_argument("--no-serial-pass", action="store_true",
                     help="skip the lookahead-off pass the roofline is taken from")
-    ap.add_argument("--cpu-real", type=int, default=16)
-    ap.add_argument("--cpu-cplx", type=int, default=16)
-    ap.add_argument("--ref-real", type=int, default=8, help="reference arm: real shifts per step")
-    ap.add_argument("--ref-cplx", type=int, default=8, help="reference arm: complex shifts per step")
+    ap.add_argument("--cpu-real", type=int, default=64)
+    ap.add_argument("--cpu-cplx", type=int, default=64)
+    ap.add_argument("--ref-real", type=int, default=None,
+                    help="reference arm: real shifts per step (default: ref_sample())")
+    ap.add_argument("--ref-cplx", type=int, default=None,
+                    help="reference arm: complex shifts per step (default: ref_sample())")
     ap.add_argument("--port", action="store_true", help="time the C oracle port, not hessrq")
     args = ap.parse_args()
     if args.impl == "reference":
