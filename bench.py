@@ -627,6 +627,11 @@ def run_gpu(args):
             line["cpu_baseline"] = {"value": a / dt, "unit": "eigenvectors/s", "cores": ref.workers,
                                     "kind": "reference", "sample": ref.sample,
                                     "converged_fraction": c / max(1, a), "port": port}
+            # BASELINE.md §5 also asks for workers = 1: a small sample (the per-core rate)
+            one = ReferenceCPU(h, er, ec, b_r, 8, 8, workers=1)
+            a1, _c1, dt1 = one.step()
+            line["cpu_baseline"]["single_worker"] = {"value": a1 / dt1, "unit": "eigenvectors/s",
+                                                     "cores": 1, "sample": one.sample}
         else:
             line["cpu_baseline"] = port
     clk_s = clk.summary()
