@@ -314,7 +314,11 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # HSRQ_BENCH_DIST=1 runs the multi-rank code path (NCCL group, collectives,
+    # the gather of X) even with one rank: `torchrun --nproc-per-node 1` on a
+    # one-GPU box exercises everything but the peer transfers
+    dist_on = world > 1 or os.environ.get("HSRQ_BENCH_DIST") == "1"
+    if dist_on:
         dist.init_process_group("nccl", device_id=dev)
 
     from paper_2101_05063_b200 import _lib
@@ -342,7 +346,7 @@ def run_gpu(args):
         return r
 
     gather_out = None
-    if world > 1:
+    if dist_on:
         from paper_2101_05063_b200.parallel import gather_columns
 
         counts = torch.tensor([gs.ncol], device=dev)
@@ -354,7 +358,7 @@ def run_gpu(args):
     def gather():
         # parallel.gather_columns: every rank's X block to rank 0 over NCCL
         # send/recv, exactly X's bytes once (what hsrq3in_distributed uses)
-        if world == 1:
+        if not dist_on:
             return
         gather_columns(gs.X, counts, dst=0, out=gather_out)
 
@@ -363,7 +367,7 @@ def run_gpu(args):
         gather()
     torch.cuda.synchronize()
     nf = lib.hsrq_failure_count(ctypes.c_void_p(gs.ws.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -381,7 +385,7 @@ def run_gpu(args):
     lib.hsrq_phase_times(ctypes.c_void_p(phase.ctypes.data))  # summed over the K timed steps
     ms = e0.elapsed_time(e1) / args.steps
     t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist_on:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
         dist.barrier()
     ms = float(t_local.item())
@@ -462,7 +466,7 @@ def run_gpu(args):
         ems_sync = ee0.elapsed_time(ee1)
         e2e_pipelined(2)
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
         ee0.record(stream)
         out = e2e_pipelined(max(1, args.steps))
@@ -470,7 +474,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         ems = ee0.elapsed_time(ee1) / max(1, args.steps)
         te = torch.tensor([ems], dtype=torch.float64, device=dev)
-        if world > 1:
+        if dist_on:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         ems = float(te.item())
         e2e = {"value": (m_total_r + m_total_c) / (ems / 1e3), "unit": "eigenvectors/s",
@@ -540,7 +544,7 @@ def run_gpu(args):
              "bound": "||Hx-lx||/(||H||_F ||x||) <= 10 n eps"}
 
     if rank != 0:
-        if world > 1:
+        if dist_on:
             dist.destroy_process_group()
         return 0
 
@@ -637,7 +641,7 @@ def run_gpu(args):
     clk_s = clk.summary()
     line["clocks"] = clk_s
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
     return 0
 
