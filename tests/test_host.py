@@ -251,3 +251,40 @@ def test_api_surface_matches_installed_reference():
         want = {m for m in dir(getattr(mod, cls)) if not m.startswith("_")}
         got = {m for m in dir(getattr(P, cls)) if not m.startswith("_")}
         assert want <= got, (cls, want - got)
+
+
+def test_committed_bench_lines_carry_the_contract_keys():
+    """The bench lines kept under profiles/ (both arms, last run of the round)
+    carry every key of the bench contract with consistent values."""
+    import json
+    import os
+
+    from conftest import ROOT
+
+    def load(name):
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.loads(f.read().strip().splitlines()[-1])
+
+    d = load("r02g_bench_final.json")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "roofline",
+              "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["dtype"] == "f64" and d["higher_is_better"] is True and d["vs_baseline"] is None
+    assert "workload" in d["config"] and "model" not in d["config"]
+    assert abs(d["value"] - 9895 / (d["ms_per_step"] / 1e3)) < 1e-6 * d["value"]
+    r = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert r["bound"] == "tensor" and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
+    assert 0.9 < r["traffic"] / r["traffic_detail"]["algorithmic_bytes"] < 1.1
+    c = d["cpu_baseline"]
+    assert c["kind"] in ("reference", "port") and c["cores"] >= 1 and "sample" in c
+    e = d["e2e"]
+    assert e["h2d_bytes_per_step"] > 2e9 and e["d2h_bytes_per_step"] > 2e9
+    assert e["value"] < d["value"]  # the transfers are inside the timed region
+    assert d["gpu_launches"] > 0 and d["clocks"]["reasons"] == []
+    ref = load("r02f_bench_reference_arm.json")
+    assert ref["impl"] == "reference" and ref["config"] == d["config"]
+    assert ref["metric"] == d["metric"] and ref["unit"] == d["unit"]
+    assert ref["e2e"]["h2d_bytes_per_step"] == 0 and ref["e2e"]["value"] == ref["value"]
